@@ -1,0 +1,160 @@
+"""ORACLE (test infrastructure only) — textbook BFV over an RNS modulus Q = prod q_l.
+
+Follows PAPER.md §2.3 (lines 236-378):
+  * symmetric encryption (c0, c1) = ([Delta m + a s + e]_Q, -a), Delta = floor(Q/t)
+    (Eq. bfv_enc, PAPER.md:244-253 [\\ignore], footnote :242);
+  * decryption [round(t [c0 + c1 s]_Q / Q)]_t, correct iff ||v||_inf < Delta/2
+    (Eq. bfv_dec2, PAPER.md:256-267 [\\ignore]);
+  * HRot = automorphism + key switching with a decomposition, hoisted
+    (decompose once, then per-rotation automorphism + key inner product; PAPER.md:373-378,
+    :1472-1473 "PermDecomp"/"PermAuto").
+Readings: RNS digits, one per limb, no special prime (R3); hoisted digit
+definition d_i = [c1]_{q_i} taken BEFORE the automorphism (R4); ternary secret and
+CBD errors come from synth/ and are passed in (R2).
+
+Ciphertexts are uint64 arrays [2][L][N] of canonical residues (coefficient form).
+Galois keys are uint64 [L digits][2: b, a][L limbs][N].
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import List, Sequence
+
+import numpy as np
+
+from . import ring
+from .params import is_prime
+
+
+@dataclass
+class BFVParams:
+    N: int
+    primes: List[int]
+    t: int
+
+    def __post_init__(self):
+        assert self.N & (self.N - 1) == 0
+        for q in self.primes:
+            assert is_prime(q) and q % (2 * self.N) == 1, q
+        assert is_prime(self.t) and self.t % (2 * self.N) == 1
+        self.Q = 1
+        for q in self.primes:
+            self.Q *= q
+        self.delta = self.Q // self.t
+
+    @property
+    def L(self) -> int:
+        return len(self.primes)
+
+
+def crt(residues: Sequence[np.ndarray], primes: Sequence[int]) -> list:
+    """x in [0, Q) with x = r_l mod q_l (Chinese remainder theorem, textbook form)."""
+    Q = 1
+    for q in primes:
+        Q *= q
+    n = len(residues[0])
+    out = [0] * n
+    for r, q in zip(residues, primes):
+        Qi = Q // q
+        c = Qi * pow(Qi, -1, q)
+        for j in range(n):
+            out[j] += int(r[j]) * c
+    return [x % Q for x in out]
+
+
+def encrypt(P: BFVParams, m, s, a, e) -> np.ndarray:
+    """Symmetric BFV encryption: c0 = [Delta m + a s + e], c1 = [-a], per limb.
+    m: [N] ints in [0,t); s: [N] ternary; a: uint64 [L][N] uniform residues; e: [N] small ints."""
+    L, N = P.L, P.N
+    ct = np.empty((2, L, N), dtype=np.uint64)
+    m = [int(x) % P.t for x in m]
+    for l, q in enumerate(P.primes):
+        a_s = ring.nc_mul(s, a[l], q)  # ternary s first: its zero terms are skipped
+        dm = np.array([(P.delta * x) % q for x in m], dtype=object)
+        ct[0, l] = ((dm + a_s.astype(object) + np.asarray(e, dtype=np.int64).astype(object)) % q).astype(np.uint64)
+        ct[1, l] = ring.canon(-(a[l].astype(object)), q)
+    return ct
+
+
+def phase(P: BFVParams, ct, s) -> list:
+    """[c0 + c1 s]_Q as integers in [0, Q)  (Eq. bfv_dec)."""
+    res = []
+    for l, q in enumerate(P.primes):
+        c1s = ring.nc_mul(s, ct[1, l], q)
+        res.append(((ct[0, l].astype(object) + c1s.astype(object)) % q))
+    return crt(res, P.primes)
+
+
+def decrypt(P: BFVParams, ct, s) -> np.ndarray:
+    """m = [round(t x / Q)]_t with x = [c0 + c1 s]_Q in [0, Q)  (Eq. bfv_dec2).
+    round(y) = floor(y + 1/2); ties cannot occur because gcd(Q, 2t) = 1."""
+    x = phase(P, ct, s)
+    return np.array([((P.t * v + P.Q // 2) // P.Q) % P.t for v in x], dtype=np.int64)
+
+
+def noise_bits(P: BFVParams, ct, s, m) -> float:
+    """log2 ||[c0 + c1 s - Delta m]_Q||_inf (centered) — the noise v of Eq. bfv_dec.
+    Decryption is correct iff this is < log2(Delta/2)  (PAPER.md:266-267 [\\ignore], :318)."""
+    import math
+    x = phase(P, ct, s)
+    worst = 0
+    for v, mm in zip(x, m):
+        r = (v - P.delta * (int(mm) % P.t)) % P.Q
+        if r > P.Q // 2:
+            r -= P.Q
+        worst = max(worst, abs(r))
+    return math.log2(worst) if worst else 0.0
+
+
+def noise_budget_bits(P: BFVParams) -> float:
+    import math
+    return math.log2(P.delta / 2)
+
+
+def galois_keygen(P: BFVParams, s, g: int, a, e) -> np.ndarray:
+    """Switching key for X -> X^g under the RNS-digit gadget (reading R3):
+    digit i, limb l:  b_{i,l} = [-a_{i,l} s + e_i + [i == l] s(X^g)]_{q_l},  a_{i,l} uniform.
+    [i == l] is the residue mod q_l of the gadget g_i = (Q/q_i)[(Q/q_i)^{-1}]_{q_i}.
+    a: uint64 [L][L][N], e: [L][N].  Returns uint64 [L][2][L][N] (b first, then a)."""
+    L, N = P.L, P.N
+    s_g = ring.automorphism(np.asarray(s, dtype=np.int64), g)
+    key = np.empty((L, 2, L, N), dtype=np.uint64)
+    for i in range(L):
+        for l, q in enumerate(P.primes):
+            a_s = ring.nc_mul(s, a[i, l], q)
+            b = -(a_s.astype(object)) + np.asarray(e[i], dtype=np.int64).astype(object)
+            if i == l:
+                b = b + s_g.astype(object)
+            key[i, 0, l] = ring.canon(b % q, q)
+            key[i, 1, l] = a[i, l]
+    return key
+
+
+def decompose(P: BFVParams, ct) -> List[np.ndarray]:
+    """Hoisting step 1 ('PermDecomp'): digits d_i = [c1]_{q_i}
+    as integer polynomials with coefficients in [0, q_i)."""
+    return [ct[1, i].astype(np.int64) for i in range(P.L)]
+
+
+def rotate_hoisted(P: BFVParams, ct, digits, g: int, key) -> np.ndarray:
+    """Hoisting step 2 ('PermAuto'): for every limb l
+        c0' = [sigma_g(c0) + sum_i sigma_g(d_i) b_{i,l}]_{q_l},   c1' = [sum_i sigma_g(d_i) a_{i,l}]_{q_l}
+    with sigma_g applied to the integer digit polynomials (reading R4)."""
+    L, N = P.L, P.N
+    dg = [ring.automorphism(d, g) for d in digits]
+    out = np.empty((2, L, N), dtype=np.uint64)
+    for l, q in enumerate(P.primes):
+        c0 = ring.automorphism_mod(ct[0, l], g, q).astype(object)
+        c1 = np.zeros(N, dtype=object)
+        for i in range(L):
+            di = ring.canon(dg[i], q)
+            c0 = c0 + ring.nc_mul(di, key[i, 0, l], q).astype(object)
+            c1 = c1 + ring.nc_mul(di, key[i, 1, l], q).astype(object)
+        out[0, l] = (c0 % q).astype(np.uint64)
+        out[1, l] = (c1 % q).astype(np.uint64)
+    return out
+
+
+def hrot(P: BFVParams, ct, g: int, key) -> np.ndarray:
+    """HRot by one automorphism (hoisted definition applied to a single rotation)."""
+    return rotate_hoisted(P, ct, decompose(P, ct), g, key)

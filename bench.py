@@ -1,0 +1,361 @@
+#!/usr/bin/env python
+"""Benchmark of the Hyena encrypted-convolution hot path on B200 (contract: see DESIGN.md §Measurement).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+
+A step = one hy_conv_eval of the configured layer (all of SURVEY §8(a): PermDecomp, PermAuto,
+lazy MAC + WHT + reduction + sign PMult, row-swap alignment, INTT) on synthetic ciphertexts
+already resident in HBM.  Default workload: BASELINE.json configs[1] (C2, ResNet-20-style layer,
+N = 8192, L = 3).  Multi-GPU (torchrun): every rank evaluates its own layer instance (weak scaling,
+no data-path collective); the time is the max over ranks.
+
+Inputs are uniformly random ciphertexts and switching keys (synth/): under RLWE a real
+encryption is indistinguishable from uniform, and the kernels' work does not depend on the values.
+bench.py never runs the oracle except in the cpu_baseline leg (rank 0, N = 1) and --impl reference.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np
+
+import synth
+
+METRIC = "encrypted conv layers/sec (ct×pt MAC GOps/s) at N=8192; % of HBM/INT roofline"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+SM_COUNT = 148
+DFMA_PER_CLK_SM = 64     # FP64 pipe: 16 lanes/clk/SMSP x 4 (tools/intbench measured 58/clk/SM at 1965 MHz nominal)
+IMAD_PER_CLK_SM = 64
+
+
+def load_peaks():
+    try:
+        return json.load(open(PEAKS_PATH))
+    except Exception:
+        return {}
+
+
+# --------------------------------------------------------------------------------------------
+# workload accounting
+# --------------------------------------------------------------------------------------------
+def layer_work(cfg, lay):
+    """Method coefficient-MACs and algorithmic bytes of one layer."""
+    L, N, T = len(cfg.primes), cfg.N, lay.n_taps
+    ctw = 2 * L * N
+    if cfg.depthwise:
+        M, K, units = (2 if lay.cn == 2 else 1), T, lay.U * lay.Jc
+    else:
+        M, K, units = (4 * lay.Jo if lay.cn == 2 else lay.Jo), lay.Jc * T, lay.U
+    mac = M * K * ctw * units                       # coefficient MACs of S3 (2 DFMA each)
+    rot = lay.J * sum(1 for s in lay.tap_step[:T] if s % (N // 2))
+    swaps = lay.Jout if (lay.cn == 2 and not cfg.depthwise) else 0
+    return dict(coef_macs=mac, dfma=2 * mac, rotations=rot, rowswaps=swaps, ct_words=ctw,
+                in_bytes=lay.J * ctw * 8, out_bytes=lay.Jout * ctw * 8, M=M, K=K, units=units)
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons through NVML while the timed region runs."""
+
+    def __init__(self, dev: int = 0, period: float = 0.005):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.period, self.dev = period, dev
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                 "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for n, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------------------------
+# GPU arm
+# --------------------------------------------------------------------------------------------
+def run_gpu(args, cfg, rank, world):
+    import torch
+    import paper_2311_12519_b200 as hy
+    from paper_2311_12519_b200 import build
+
+    if rank == 0 or not os.path.exists(hy.library_path()):
+        build.build()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    dev = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(dev)
+    lay0 = hy.hy_plan_layout(cfg.N, cfg.t, **cfg.shape_dict())
+    L = len(cfg.primes)
+    p = hy.hy_params_create(cfg.N, cfg.primes, cfg.t, dev)
+    elts = list(lay0.galois[:lay0.n_galois])
+    keys = synth.gen_uniform_keys(cfg.primes, len(elts), cfg.N, cfg.index, stream=rank)
+    hy.hy_keys_upload(p, elts, keys)
+    W = synth.gen_weights(cfg)
+    w = hy.hy_encode_weights(p, W, **cfg.shape_dict())
+    lay = hy.hy_weights_layout(w)
+    work = layer_work(cfg, lay)
+    J, Jout = lay.J, lay.Jout
+    ct_host = synth.gen_uniform_cts(cfg.primes, J, cfg.N, cfg.index, stream=rank)
+    ct_in = torch.from_numpy(ct_host).to(f"cuda:{dev}")
+    ct_out = torch.empty((Jout, 2, L, cfg.N), dtype=torch.uint64, device=f"cuda:{dev}")
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=f"cuda:{dev}")  # > 126 MB L2
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    hy.hy_weights_set_stage_events(w, ev)
+    for _ in range(args.warmup):
+        hy.hy_conv_eval(w, ct_in, ct_out)
+    torch.cuda.synchronize()
+
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms, stage_ms = [], [[] for _ in range(4)]
+    launches0 = hy.hy_kernel_launches()
+    with ClockSampler(dev) as clk:
+        for _ in range(args.steps):
+            flush.zero_()                       # L2 flushed between timed iterations (untimed)
+            hy.hy_conv_eval(w, ct_in, ct_out)
+            ev[4].synchronize()
+            step_ms.append(ev[0].elapsed_time(ev[4]))
+            for i in range(4):
+                stage_ms[i].append(ev[i].elapsed_time(ev[i + 1]))
+    torch.cuda.synchronize()
+    launches = hy.hy_kernel_launches() - launches0
+    total_ms = sum(step_ms)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+
+    # end-to-end through the public host API: H2D of inputs and D2H of outputs inside the timing
+    hy.hy_weights_set_stage_events(w, [])
+    pin_in = torch.from_numpy(ct_host).pin_memory().numpy()
+    pin_out = torch.empty((Jout, 2, L, cfg.N), dtype=torch.uint64).pin_memory().numpy()
+    for _ in range(2):
+        hy.hy_conv_eval_host(w, pin_in, pin_out)
+    e2e_steps = max(3, min(args.steps, 50))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        hy.hy_conv_eval_host(w, pin_in, pin_out)   # synchronises the stream before returning
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    hy.hy_weights_destroy(w)
+    hy.hy_params_destroy(p)
+    return dict(total_ms=total_ms, step_ms=step_ms, stage_ms=[statistics.mean(s) for s in stage_ms],
+                launches=launches, clocks=clk.summary(), work=work, lay=lay, e2e_s=e2e_s, e2e_steps=e2e_steps)
+
+
+def roofline(cfg, res, peaks):
+    """Roofline of the dominant stage (largest mean time)."""
+    w = res["work"]
+    names = ["S1_permdecomp", "S2_permauto", "S3_mac_wht", "S4S5_align_intt"]
+    st = res["stage_ms"]
+    dom = int(np.argmax(st))
+    clk = res["clocks"]
+    clk_mhz = peaks.get("sm_max_mhz", 1965.0)
+    if dom == 2:
+        achieved = w["dfma"] / (st[2] * 1e-3) / 1e12
+        peak = DFMA_PER_CLK_SM * SM_COUNT * clk_mhz * 1e6 / 1e12
+        return {"kernel": names[dom], "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TDFMA/s",
+                "frac": achieved / peak, "traffic": None,
+                "peak_note": f"FP64 pipe {DFMA_PER_CLK_SM}/clk/SM x {SM_COUNT} SMs x sm_max {clk_mhz:.0f} MHz "
+                             "(derived; DESIGN.md)"}
+    L, N = len(cfg.primes), cfg.N
+    lay = res["lay"]
+    if dom == 1:
+        T = lay.n_taps
+        # per rotated coefficient: read L digits + C0 (gathered), 2L key words + 2L Shoup words, write 2
+        bytes_ = lay.J * T * L * N * 8 * ((L + 1) + 4 * L + 2)
+    elif dom == 0:
+        bytes_ = lay.J * (2 * L * N * 8 + (L * L + L) * N * 8)
+    else:
+        bytes_ = lay.Jout * (3 * 2 * L * N * 8)
+    hbm = peaks.get("hbm_gbs", 6547.2)
+    achieved = bytes_ / (st[dom] * 1e-3) / 1e9
+    return {"kernel": names[dom], "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": None}
+
+
+# --------------------------------------------------------------------------------------------
+# CPU oracle (cpu_baseline leg and --impl reference)
+# --------------------------------------------------------------------------------------------
+def oracle_sample(cfg, budget_s: float = 20.0):
+    """Time the oracle as it stands on a bounded sample of the layer: one input ciphertext's
+    PermDecomp + one hoisted rotation, and one output group's MAC/WHT/sign/(row swap) — then
+    extrapolate linearly to the layer's rotation and output counts.  Returns (layers/s, desc)."""
+    from oracle import bfv, conv
+    from oracle.params import galois_elt_for_step, rowswap_elt
+    P = bfv.BFVParams(cfg.N, cfg.primes, cfg.t)
+    p = conv.plan(cfg.N, cfg.batch, cfg.Ci, cfg.Co, cfg.H, cfg.W, cfg.kh, cfg.kw, cfg.pad, cfg.depthwise,
+                  cfg.force_cn)
+    ls = conv.setup(p, cfg.t)
+    L = P.L
+    ct = synth.gen_uniform_cts(cfg.primes, 1, cfg.N, cfg.index)[0]
+    key = synth.gen_uniform_keys(cfg.primes, 1, cfg.N, cfg.index)[0]
+    step = next(s for _, _, s in p.taps if s % (cfg.N // 2))
+    g = galois_elt_for_step(cfg.N, step)
+    t0 = time.perf_counter()
+    d = bfv.decompose(P, ct)
+    bfv.rotate_hoisted(P, ct, d, g, key)
+    t_rot = time.perf_counter() - t0
+    # one output group's MAC over its K terms (uses the same ct for every term: timing only)
+    W = synth.gen_weights(cfg)
+    T = len(p.taps)
+    K = T if cfg.depthwise else p.Jc * T
+    t0 = time.perf_counter()
+    nB = 1 if p.cn == 1 else (2 if cfg.depthwise else 4)
+    for _ in range(nB):
+        conv._lincomb(P, [(int(W.flat[i % W.size]) or 1, ct) for i in range(K)])
+    if p.cn == 2:
+        from oracle import ring
+        S = conv.sign_poly(P, ls)
+        for _ in range(1 if cfg.depthwise else 2):
+            for comp in range(2):
+                for l, q in enumerate(P.primes):
+                    ring.nc_mul(S[l], ct[comp, l], q)
+    t_mac = time.perf_counter() - t0
+    n_rot = p.J * sum(1 for _, _, s in p.taps if s % (cfg.N // 2))
+    n_swap = p.Jout if (p.cn == 2 and not cfg.depthwise) else 0
+    n_groups = p.Jout
+    t_layer = (n_rot + n_swap) * t_rot + n_groups * t_mac
+    desc = (f"1 hoisted rotation ({t_rot:.2f} s) + 1 output group's MAC/WHT/sign ({t_mac:.2f} s), "
+            f"extrapolated x{n_rot + n_swap} rotations and x{n_groups} groups; single thread")
+    return 1.0 / t_layer, desc, t_rot + t_mac
+
+
+def run_reference(args, cfg):
+    import torch
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    samples, desc = [], ""
+    for i in range(args.warmup + args.steps):
+        v, desc, _ = oracle_sample(cfg)
+        if i >= args.warmup:
+            samples.append(v)
+    v = statistics.median(samples)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "layers/s",
+            "n_gpus": int(os.environ.get("WORLD_SIZE", 1)), "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "int (Python/NumPy + C schoolbook)", "data": "synthetic",
+            "config": {"workload": cfg.name, "N": cfg.N, "L": len(cfg.primes)},
+            "cpu_baseline": {"value": v, "unit": "layers/s", "cores": 1, "kind": "oracle", "sample": desc},
+            "e2e": {"value": v, "unit": "layers/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="hyena", choices=["hyena", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 3, "W >= 3 warm-up steps"
+    cfg = synth.configs()[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    rank = int(os.environ.get("RANK", 0))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    res = run_gpu(args, cfg, rank, world)
+    if rank == 0:
+        peaks = load_peaks()
+        work, lay = res["work"], res["lay"]
+        ms = res["total_ms"] / args.steps
+        layers_s = world * args.steps / (res["total_ms"] * 1e-3)
+        gops = layers_s * work["coef_macs"] / 1e9
+        e2e = world * res["e2e_steps"] / res["e2e_s"]
+        line = {
+            "metric": METRIC, "value": layers_s, "unit": "layers/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64 (exact modular int; MAC on the FP64 pipe, exact)",
+            "data": "synthetic (uniform ciphertexts + keys; RLWE-indistinguishable from real ones)",
+            "config": {"workload": f"{cfg.name}: Ci={cfg.Ci} Co={cfg.Co} H=W={cfg.H} {cfg.kh}x{cfg.kw} pad={cfg.pad} "
+                                   f"batch={cfg.batch} depthwise={cfg.depthwise}",
+                       "N": cfg.N, "L": len(cfg.primes), "t": cfg.t, "c_n": lay.cn, "k": lay.k, "J": lay.J,
+                       "Jout": lay.Jout, "rotations": work["rotations"], "rowswaps": work["rowswaps"],
+                       "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"replicas x{world}"},
+            "ct_mac_gops": gops,
+            "stages_ms": dict(zip(["S1_permdecomp", "S2_permauto", "S3_mac_wht", "S4S5_align_intt"],
+                                  res["stage_ms"])),
+            "roofline": roofline(cfg, res, peaks),
+            "gpu_launches": res["launches"],
+            "clocks": res["clocks"],
+            "e2e": {"value": e2e, "unit": "layers/s", "h2d_bytes_per_step": work["in_bytes"],
+                    "d2h_bytes_per_step": work["out_bytes"]},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            v, desc, _ = oracle_sample(cfg)
+            line["cpu_baseline"] = {"value": v, "unit": "layers/s", "cores": 1, "kind": "oracle", "sample": desc}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,168 @@
+/*
+ * hyena.h — C-ABI of the B200 (sm_100a) implementation of the server-side hot path of
+ * "Hyena: Optimizing Homomorphically Encrypted Convolution for Private CNN Inference"
+ * (arXiv 2311.12519; /root/reference/PAPER.md).
+ *
+ * The server receives input ciphertexts, holds switching keys for HRot and model weights
+ * prepared offline, and returns output ciphertexts packing the output channels
+ * (PAPER.md:883-884, 1590-1594).  The calls below follow that problem statement.
+ *
+ * Conventions for every call:
+ *   - Status codes only (hy_status); no C++ exception crosses the ABI.  On failure the
+ *     thread-local message hy_last_error() says why.
+ *   - Ciphertexts are BFV pairs (c0, c1) over Q = prod q_l (RNS, L limbs), ring
+ *     Z_q[X]/(X^N+1) (PAPER.md:276-280 [\ignore]), stored limb-major uint64
+ *     [2][L][N] in COEFFICIENT form with canonical residues in [0, q_l)
+ *     (reading R18) — both on input and on output.
+ *   - Ciphertext buffers are caller-owned device memory (e.g. torch tensors); the library
+ *     never frees them.  Handles are opaque and owned by the library.
+ *   - Params, keys and weights are immutable after creation, except that a hy_weights
+ *     owns the workspace of hy_conv_eval: one evaluation at a time per hy_weights.
+ *   - Device calls are stream-ordered on the given cudaStream_t (void*; NULL = legacy
+ *     default stream) and do not synchronise the host except where stated.
+ */
+#ifndef HYENA_H_
+#define HYENA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t hy_status;
+#define HY_OK 0
+#define HY_EINVAL (-1)  /* bad argument (non-prime modulus, N not a power of two, ...) */
+#define HY_ENOMEM (-2)  /* device or host allocation failed */
+#define HY_ECUDA (-3)   /* a CUDA runtime call or kernel launch failed */
+#define HY_ENOKEY (-4)  /* a Galois key the layout needs was not uploaded */
+#define HY_ESHAPE (-5)  /* ciphertext counts / shapes do not match the layout */
+
+#define HY_MAX_LIMBS 8
+#define HY_MAX_TAPS 49     /* kernels up to 7x7 */
+#define HY_MAX_GALOIS 64
+
+typedef struct hy_params hy_params;
+typedef struct hy_weights hy_weights;
+
+/* One convolution layer: stride 1, zero padding `pad`, cross-correlation
+ * out[b,o,y,x] = sum_{c,dy,dx} W[o,c,dy,dx] x[b,c,y+dy-pad,x+dx-pad].
+ * depthwise != 0: W is [C][kh][kw] and output channel o reads input channel o only.
+ * k = 0 selects the paper's k (argmin_{1<=k<=32} |[k h]_t|; reading R13);
+ * force_cn = 0 chooses c_n automatically (reading R10), else 1 or 2. */
+typedef struct {
+  uint32_t Ci, Co, H, W, kh, kw, pad, stride, depthwise, batch;
+  int32_t k, force_cn;
+} hy_conv_shape;
+
+/* Layout chosen for a layer (readings R8-R10, R15):
+ *   Wp = next_pow2(W + 2 pad), Hp = next_pow2(H + 2 pad);
+ *   mode 0 ("blocks"): per_row images of Hp x Wp per slot row (N/2 slots);
+ *   mode 1 ("bands"):  Hb = (N/2)/Wp rows per band, Hv = Hb - (kh-1) valid rows,
+ *                      `bands` bands per image (halo rows duplicated by the client);
+ *   G slot-row groups per channel; cn channels per ciphertext (1 or 2);
+ *   U independent units, each with Jc input and Jo output ciphertexts
+ *   (cn = 2: input ct u*Jc + j holds channels 2j (row 0) and 2j+1 (row 1) of group u;
+ *    cn = 1: input ct u*Jc + c holds channel c, groups 2u (row 0) and 2u+1 (row 1));
+ *   taps (dy, dx) row-major with left-rotation step (dy-pad)*Wp + (dx-pad);
+ *   output slots = (c_n k) * conv (scale), remove with scale^{-1} mod t (reading R12);
+ *   galois[] = Galois elements whose keys hy_conv_eval needs (taps, then row swap). */
+typedef struct {
+  uint32_t N, L;
+  uint32_t Hout, Wout, Wp, Hp, mode, per_row, Hb, Hv, bands, G, cn, U, Jc, Jo, J, Jout;
+  uint32_t n_taps;
+  int32_t tap_dy[HY_MAX_TAPS], tap_dx[HY_MAX_TAPS], tap_step[HY_MAX_TAPS];
+  uint32_t k, scale, h;
+  int32_t sign_coeff;           /* centered [k h]_t: the [k,-k] plaintext's two coefficients */
+  uint32_t n_galois;
+  uint32_t galois[HY_MAX_GALOIS];
+} hy_layout;
+
+/* Thread-local message describing the last failing call ("" if none). */
+const char* hy_last_error(void);
+
+/* Host-only layout planner (no device needed).  t is the plaintext modulus.
+ * Errors: HY_EINVAL (N not a power of two in [16, 65536], t not prime or t != 1 mod 2N),
+ * HY_ESHAPE (stride != 1, kernel larger than the padded input, a band shorter than the
+ * kernel, too many taps). */
+hy_status hy_plan_layout(uint32_t N, uint64_t t, const hy_conv_shape* shape, hy_layout* out);
+
+/* Create ring parameters on CUDA device `device` (PAPER.md:611 step 1: q = p = 1 mod 2N).
+ * q_primes[L] (host): distinct primes 2^20 < q_l < 2^60, q_l = 1 mod 2N; t prime, t = 1 mod 2N,
+ * t not among q_l; N a power of two in [1024, 16384]; 1 <= L <= HY_MAX_LIMBS.
+ * Builds the per-limb Shoup twiddle tables (bit-reversed psi powers), the plaintext slot
+ * tables (zeta_t = least primitive 2N-th root mod t; reading A1) and uploads them.
+ * Errors: HY_EINVAL, HY_ENOMEM, HY_ECUDA.  *out is set only on success. */
+hy_status hy_params_create(uint32_t N, const uint64_t* q_primes, uint32_t L, uint64_t t, int device,
+                           hy_params** out);
+void hy_params_destroy(hy_params* p);
+
+/* Upload server-side switching keys generated by the client (PAPER.md:883-884, 1474-1475 [app]).
+ * keys: [n_elts][L digits][2: b, a][L limbs][N] uint64, COEFFICIENT form, canonical residues;
+ * key for element g satisfies b_{i,l} + a_{i,l} s = e_i + [i == l] s(X^g)  (mod q_l)
+ * (RNS-digit gadget, reading R3).  keys_on_device != 0: `keys` is a device pointer.
+ * The library converts them to NTT form with Shoup companions and keeps its own copy;
+ * re-uploading an element replaces it.  Synchronises the device.  Errors: HY_EINVAL
+ * (even or out-of-range element, too many elements), HY_ENOMEM, HY_ECUDA. */
+hy_status hy_keys_upload(hy_params* p, uint32_t n_elts, const uint32_t* galois_elts, const uint64_t* keys,
+                         int keys_on_device);
+
+/* Prepare one layer: plans the layout, picks k, builds the
+ * [k, -k] sign plaintext ([k h]_t at X^{N/4} and X^{3N/4}, centered lift)
+ * in NTT form, and the int weight tables; allocates the evaluation workspace for U units.
+ * W (host, int8): [Co][Ci][kh][kw], or [C][kh][kw] when depthwise.
+ * Errors: HY_EINVAL, HY_ESHAPE, HY_ENOMEM, HY_ECUDA.  Synchronises the device. */
+hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* shape, const int8_t* W, hy_weights** out);
+hy_status hy_weights_layout(const hy_weights* w, hy_layout* out);
+void hy_weights_destroy(hy_weights* w);
+
+/* The encrypted convolution (CNNLayer/ProposedConv):
+ * hoisted rotations of every input ciphertext by every tap step (PermDecomp + PermAuto),
+ * lazy multiply-accumulate of the int weights with one reduction per output
+ * (PAPER.md:718-728), Walsh-Hadamard butterflies + [k,-k] PMult for c_n = 2 (Eq. 2,
+ * PAPER.md:532-560), alignment of diagonal 1 by the row-swap HRot,
+ * and the return to coefficient form.
+ * ct_in: device [J][2][L][N] with J = nu * Jc for 1 <= nu <= U units (unit-major, see
+ * hy_layout); ct_out: device [Jout][2][L][N], Jout = nu * Jo.  Output slots hold
+ * scale * conv (mod t).  Stream-ordered, no host sync.  Errors: HY_ESHAPE, HY_ENOKEY,
+ * HY_ECUDA. */
+hy_status hy_conv_eval(hy_weights* w, const uint64_t* ct_in, size_t J, uint64_t* ct_out, size_t Jout,
+                       void* cuda_stream);
+
+/* Same computation from/to HOST buffers (pinned or pageable): copies ct_in to the device,
+ * evaluates, copies ct_out back, and synchronises the stream before returning. */
+hy_status hy_conv_eval_host(hy_weights* w, const uint64_t* ct_in_host, size_t J, uint64_t* ct_out_host,
+                            size_t Jout, void* cuda_stream);
+
+/* Per-stage entry points (for per-kernel parity tests; same kernels as hy_conv_eval).
+ * hy_poly_mul: c = a * b in Z_{q_l}[X]/(X^N+1) for n polynomial pairs, all device
+ *   [n][L][N] coefficient form (forward NTT, pointwise Shoup product, inverse NTT).
+ * hy_ntt_roundtrip: x -> INTT(NTT(x)) in place, device [n][L][N].
+ * hy_rotate: hoisted HRot of n ciphertexts by Galois element g (key must be uploaded):
+ *   device [n][2][L][N] -> device [n][2][L][N], coefficient form. */
+hy_status hy_poly_mul(const hy_params* p, const uint64_t* a, const uint64_t* b, uint64_t* c, size_t n,
+                      void* cuda_stream);
+hy_status hy_ntt_roundtrip(const hy_params* p, uint64_t* x, size_t n, void* cuda_stream);
+hy_status hy_rotate(hy_params* p, const uint64_t* ct_in, uint32_t galois_elt, uint64_t* ct_out, size_t n,
+                    void* cuda_stream);
+
+/* Measurement hooks (bench.py): total number of kernels this library has launched in the
+ * process, and optional CUDA events (cudaEvent_t cast to void*) that hy_conv_eval records on
+ * its stream at the stage boundaries [before S1, after S1, after S2, after S3, after S4+S5].
+ * n = 0 clears them.  Errors: HY_EINVAL. */
+uint64_t hy_kernel_launches(void);
+hy_status hy_weights_set_stage_events(hy_weights* w, void* const* events, uint32_t n);
+
+/* Debug decryption (PAPER.md:256-267 [\ignore]): for each of n device ciphertexts
+ * [n][2][L][N] computes [c0 + c1 s]_{q_l} on the GPU, then on the host the exact CRT
+ * rounding m = [round(t x / Q)]_t, slot decoding and multiplication by
+ * scale^{-1} mod t.  sk: host ternary int8 [N].  slots_out: host [n][N] in slot order
+ * (row 0 slots 0..N/2-1, then row 1).  Not on the hot path; synchronises the device. */
+hy_status hy_decrypt_debug(const hy_params* p, const int8_t* sk, const uint64_t* ct, size_t n, uint32_t scale,
+                           uint64_t* slots_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HYENA_H_ */

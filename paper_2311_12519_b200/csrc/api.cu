@@ -1,0 +1,799 @@
+// C-ABI entry points of include/hyena.h and the library's host-side logic (parameter tables,
+// layout planner, weight encoding, debug decryption).  Independent of oracle/ by construction:
+// every formula is re-derived from PAPER.md here.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "hy_common.cuh"
+
+// ============================================================================================
+// errors
+// ============================================================================================
+static thread_local char g_err[1024] = "";
+
+void hy_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+extern "C" const char* hy_last_error(void) { return g_err; }
+
+#include <atomic>
+static std::atomic<uint64_t> g_launches{0};
+void hy_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+extern "C" uint64_t hy_kernel_launches(void) { return g_launches.load(); }
+
+#define HY_CHECK(cond, code, ...) \
+  do {                            \
+    if (!(cond)) {                \
+      hy_set_error(__VA_ARGS__);  \
+      return code;                \
+    }                             \
+  } while (0)
+
+// ============================================================================================
+// host number theory
+// ============================================================================================
+namespace hyhost {
+u64 mulmod(u64 a, u64 b, u64 m) { return (u64)((u128)a * b % m); }
+u64 powmod(u64 a, u64 e, u64 m) {
+  u64 r = 1 % m;
+  a %= m;
+  while (e) {
+    if (e & 1) r = mulmod(r, a, m);
+    a = mulmod(a, a, m);
+    e >>= 1;
+  }
+  return r;
+}
+u64 invmod(u64 a, u64 m) {  // m prime
+  return powmod(a, m - 2, m);
+}
+bool is_prime(u64 n) {
+  if (n < 2) return false;
+  static const u64 small[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  for (u64 p : small)
+    if (n % p == 0) return n == p;
+  u64 d = n - 1;
+  int r = 0;
+  while ((d & 1) == 0) {
+    d >>= 1;
+    r++;
+  }
+  for (u64 a : small) {
+    u64 x = powmod(a, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool comp = true;
+    for (int i = 1; i < r; i++) {
+      x = mulmod(x, x, n);
+      if (x == n - 1) {
+        comp = false;
+        break;
+      }
+    }
+    if (comp) return false;
+  }
+  return true;
+}
+u64 shoup(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
+uint32_t bitrev(uint32_t x, uint32_t bits) {
+  uint32_t r = 0;
+  for (uint32_t i = 0; i < bits; i++) r |= ((x >> i) & 1u) << (bits - 1 - i);
+  return r;
+}
+// a primitive 2N-th root of unity mod q (q prime, q = 1 mod 2N)
+u64 root_2n(u64 q, uint32_t N) {
+  for (u64 x = 2; x < q; x++) {
+    u64 psi = powmod(x, (q - 1) / (2 * (u64)N), q);
+    if (powmod(psi, N, q) == q - 1) return psi;
+  }
+  return 0;
+}
+}  // namespace hyhost
+
+using namespace hyhost;
+
+static uint32_t next_pow2(uint32_t x) {
+  uint32_t r = 1;
+  while (r < x) r <<= 1;
+  return r;
+}
+
+static int64_t centered(u64 x, u64 t) { return x > t / 2 ? (int64_t)x - (int64_t)t : (int64_t)x; }
+
+// ============================================================================================
+// layout planner (readings R8-R10, R15)
+// ============================================================================================
+static bool valid_N(uint32_t N) { return N >= 16 && N <= 65536 && (N & (N - 1)) == 0; }
+
+extern "C" hy_status hy_plan_layout(uint32_t N, uint64_t t, const hy_conv_shape* sh, hy_layout* out) {
+  HY_CHECK(sh && out, HY_EINVAL, "null argument");
+  HY_CHECK(valid_N(N), HY_EINVAL, "N=%u must be a power of two in [16, 65536]", N);
+  HY_CHECK(is_prime(t) && (t - 1) % (2 * (u64)N) == 0, HY_EINVAL, "t=%llu must be a prime = 1 mod 2N",
+           (unsigned long long)t);
+  HY_CHECK(sh->stride == 1, HY_ESHAPE, "only stride 1 is supported (got %u)", sh->stride);
+  HY_CHECK(sh->Ci >= 1 && sh->H >= 1 && sh->W >= 1 && sh->kh >= 1 && sh->kw >= 1 && sh->batch >= 1, HY_ESHAPE,
+           "empty shape");
+  HY_CHECK(sh->depthwise || sh->Co >= 1, HY_ESHAPE, "Co must be >= 1");
+  HY_CHECK(!sh->depthwise || sh->Co == sh->Ci || sh->Co == 0, HY_ESHAPE, "depthwise needs Co == Ci");
+  HY_CHECK(sh->force_cn == 0 || sh->force_cn == 1 || sh->force_cn == 2, HY_EINVAL, "force_cn must be 0, 1 or 2");
+  hy_layout L;
+  memset(&L, 0, sizeof(L));
+  L.N = N;
+  const uint32_t row = N / 2;
+  const int64_t Hout = (int64_t)sh->H + 2 * sh->pad - sh->kh + 1, Wout = (int64_t)sh->W + 2 * sh->pad - sh->kw + 1;
+  HY_CHECK(Hout > 0 && Wout > 0, HY_ESHAPE, "kernel larger than the padded input");
+  HY_CHECK(sh->kh * sh->kw <= HY_MAX_TAPS, HY_ESHAPE, "at most %d taps", HY_MAX_TAPS);
+  L.Hout = (uint32_t)Hout;
+  L.Wout = (uint32_t)Wout;
+  L.Wp = next_pow2(sh->W + 2 * sh->pad);
+  L.Hp = next_pow2(sh->H + 2 * sh->pad);
+  if ((u64)L.Hp * L.Wp <= row) {
+    L.mode = 0;
+    L.per_row = row / (L.Hp * L.Wp);
+    L.bands = 1;
+    L.G = (sh->batch + L.per_row - 1) / L.per_row;
+  } else {
+    HY_CHECK(L.Wp <= row, HY_ESHAPE, "padded width %u exceeds a slot row (%u)", L.Wp, row);
+    L.mode = 1;
+    L.Hb = row / L.Wp;
+    HY_CHECK(L.Hb > sh->kh - 1, HY_ESHAPE, "band of %u rows too short for kh=%u", L.Hb, sh->kh);
+    L.Hv = L.Hb - (sh->kh - 1);
+    L.bands = (L.Hout + L.Hv - 1) / L.Hv;
+    L.G = sh->batch * L.bands;
+  }
+  L.cn = sh->force_cn ? (uint32_t)sh->force_cn : (L.G <= 1 ? 2u : 1u);
+  const uint32_t C = sh->Ci;
+  if (L.cn == 2) {
+    L.U = L.G;
+    L.Jc = (C + 1) / 2;
+    L.Jo = sh->depthwise ? L.Jc : (sh->Co + 1) / 2;
+  } else {
+    L.U = (L.G + 1) / 2;
+    L.Jc = C;
+    L.Jo = sh->depthwise ? C : sh->Co;
+  }
+  L.J = L.U * L.Jc;
+  L.Jout = L.U * L.Jo;
+  L.n_taps = sh->kh * sh->kw;
+  for (uint32_t dy = 0; dy < sh->kh; dy++)
+    for (uint32_t dx = 0; dx < sh->kw; dx++) {
+      const uint32_t tau = dy * sh->kw + dx;
+      L.tap_dy[tau] = (int32_t)dy;
+      L.tap_dx[tau] = (int32_t)dx;
+      L.tap_step[tau] = ((int32_t)dy - (int32_t)sh->pad) * (int32_t)L.Wp + ((int32_t)dx - (int32_t)sh->pad);
+    }
+  // Hadamard scale: h = -(w + w^3)/2, w = zeta^{N/4}, zeta = least primitive
+  // 2N-th root mod t; k = argmin_{1<=k<=32} |[k h]_t|, ties to the smaller k (reading R13).
+  u64 zeta = 0;
+  for (u64 x = 2; x < t; x++)
+    if (powmod(x, N, t) == t - 1) {
+      zeta = x;
+      break;
+    }
+  const u64 w = powmod(zeta, N / 4, t);
+  const u64 s = (w + powmod(w, 3, t)) % t;
+  const u64 h = mulmod((t - s) % t, invmod(2, t), t);
+  L.h = (uint32_t)h;
+  if (L.cn == 2) {
+    uint32_t k = 0;
+    if (sh->k > 0) {
+      k = (uint32_t)sh->k;
+    } else {
+      int64_t best = -1;
+      for (uint32_t kk = 1; kk <= 32; kk++) {
+        int64_t v = centered(mulmod(kk, h, t), t);
+        v = v < 0 ? -v : v;
+        if (best < 0 || v < best) {
+          best = v;
+          k = kk;
+        }
+      }
+    }
+    HY_CHECK(k >= 1 && k <= 32, HY_EINVAL, "k must be in [1, 32] (got %d)", sh->k);
+    L.k = k;
+    L.scale = 2 * k;
+    L.sign_coeff = (int32_t)centered(mulmod(k, h, t), t);
+  } else {
+    L.k = 1;
+    L.scale = 1;
+    L.sign_coeff = 0;
+  }
+  // Galois elements: left rotation by s <-> X -> X^{3^{s mod N/2}} (reading R7)
+  L.n_galois = 0;
+  auto add_g = [&](uint32_t g) {
+    for (uint32_t i = 0; i < L.n_galois; i++)
+      if (L.galois[i] == g) return;
+    L.galois[L.n_galois++] = g;
+  };
+  for (uint32_t tau = 0; tau < L.n_taps; tau++) {
+    const int64_t st = ((int64_t)L.tap_step[tau] % (int64_t)row + row) % row;
+    if (st != 0) add_g((uint32_t)powmod(3, (u64)st, 2 * (u64)N));
+  }
+  if (L.cn == 2 && !sh->depthwise) add_g(2 * N - 1);
+  // exactness bounds of the FP64-pipe accumulation
+  const u64 K = sh->depthwise ? L.n_taps : (u64)L.Jc * L.n_taps;
+  HY_CHECK(K <= 65536, HY_ESHAPE, "MAC depth %llu exceeds 2^16", (unsigned long long)K);
+  HY_CHECK(L.cn == 1 || K * L.k <= (1u << 21), HY_ESHAPE, "MAC depth x k too large for exact accumulation");
+  *out = L;
+  return HY_OK;
+}
+
+// ============================================================================================
+// params
+// ============================================================================================
+static hy_status upload(void** dst, const void* src, size_t bytes) {
+  HY_CUDA_TRY(cudaMalloc(dst, bytes));
+  HY_CUDA_TRY(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
+  return HY_OK;
+}
+
+extern "C" hy_status hy_params_create(uint32_t N, const uint64_t* q, uint32_t L, uint64_t t, int device,
+                                      hy_params** out) {
+  HY_CHECK(out && q, HY_EINVAL, "null argument");
+  HY_CHECK(N >= 1024 && N <= 16384 && (N & (N - 1)) == 0, HY_EINVAL, "N=%u must be a power of two in [1024, 16384]",
+           N);
+  HY_CHECK(L >= 1 && L <= HY_MAX_LIMBS, HY_EINVAL, "L=%u must be in [1, %d]", L, HY_MAX_LIMBS);
+  HY_CHECK(is_prime(t) && (t - 1) % (2 * (u64)N) == 0, HY_EINVAL, "t must be a prime = 1 mod 2N");
+  for (uint32_t l = 0; l < L; l++) {
+    HY_CHECK(q[l] > (1ull << 20) && q[l] < (1ull << 60), HY_EINVAL, "q[%u] must be in (2^20, 2^60)", l);
+    HY_CHECK(is_prime(q[l]), HY_EINVAL, "q[%u]=%llu is not prime", l, (unsigned long long)q[l]);
+    HY_CHECK((q[l] - 1) % (2 * (u64)N) == 0, HY_EINVAL, "q[%u] != 1 mod 2N", l);
+    HY_CHECK(q[l] != t, HY_EINVAL, "q[%u] equals t", l);
+    for (uint32_t m = 0; m < l; m++) HY_CHECK(q[m] != q[l], HY_EINVAL, "duplicate prime");
+  }
+  HY_CUDA_TRY(cudaSetDevice(device));
+  hy_params* p = new hy_params();
+  p->N = N;
+  p->logN = 0;
+  while ((1u << p->logN) < N) p->logN++;
+  p->L = L;
+  p->t = t;
+  p->device = device;
+  std::vector<u64> psi_rev((size_t)L * N), psi_rev_sh((size_t)L * N), ipsi_rev((size_t)L * N),
+      ipsi_rev_sh((size_t)L * N);
+  for (uint32_t l = 0; l < L; l++) {
+    const u64 ql = q[l];
+    p->q[l] = ql;
+    const u64 psi = root_2n(ql, N);
+    const u64 ipsi = invmod(psi, ql);
+    for (uint32_t k = 0; k < N; k++) {
+      const uint32_t br = bitrev(k, p->logN);
+      const u64 w = powmod(psi, br, ql), iw = powmod(ipsi, br, ql);
+      psi_rev[(size_t)l * N + k] = w;
+      psi_rev_sh[(size_t)l * N + k] = shoup(w, ql);
+      ipsi_rev[(size_t)l * N + k] = iw;
+      ipsi_rev_sh[(size_t)l * N + k] = shoup(iw, ql);
+    }
+    LimbConst& c = p->lc[l];
+    c.q = ql;
+    c.two_q = 2 * ql;
+    c.ninv = invmod(N % ql, ql);
+    c.ninv_sh = shoup(c.ninv, ql);
+    c.one_sh = shoup(1, ql);
+    c.c30 = (1ull << 30) % ql;
+    c.c30_sh = shoup(c.c30, ql);
+    c.off = ql * (((1ull << 59) + ql - 1) / ql);
+  }
+  const size_t bytes = (size_t)L * N * sizeof(u64);
+  hy_status st;
+  if ((st = upload((void**)&p->tab.psi_rev, psi_rev.data(), bytes)) != HY_OK ||
+      (st = upload((void**)&p->tab.psi_rev_sh, psi_rev_sh.data(), bytes)) != HY_OK ||
+      (st = upload((void**)&p->tab.ipsi_rev, ipsi_rev.data(), bytes)) != HY_OK ||
+      (st = upload((void**)&p->tab.ipsi_rev_sh, ipsi_rev_sh.data(), bytes)) != HY_OK) {
+    hy_params_destroy(p);
+    return st;
+  }
+  p->zeta_t = 0;
+  for (u64 x = 2; x < t; x++)
+    if (powmod(x, N, t) == t - 1) {
+      p->zeta_t = x;
+      break;
+    }
+  *out = p;
+  return HY_OK;
+}
+
+extern "C" void hy_params_destroy(hy_params* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  cudaFree(p->tab.psi_rev);
+  cudaFree(p->tab.psi_rev_sh);
+  cudaFree(p->tab.ipsi_rev);
+  cudaFree(p->tab.ipsi_rev_sh);
+  for (auto& kv : p->keys) cudaFree(kv.second.ntt);
+  delete p;
+}
+
+extern "C" hy_status hy_keys_upload(hy_params* p, uint32_t n, const uint32_t* elts, const uint64_t* keys,
+                                    int keys_on_device) {
+  HY_CHECK(p && (n == 0 || (elts && keys)), HY_EINVAL, "null argument");
+  HY_CUDA_TRY(cudaSetDevice(p->device));
+  const size_t L = p->L, N = p->N;
+  const size_t key_words = L * 2 * L * N;
+  u64* tmp = nullptr;
+  HY_CUDA_TRY(cudaMalloc(&tmp, key_words * sizeof(u64)));
+  for (uint32_t e = 0; e < n; e++) {
+    const uint32_t g = elts[e];
+    if (!(g & 1) || g >= 2 * p->N) {
+      cudaFree(tmp);
+      hy_set_error("Galois element %u must be odd and < 2N", g);
+      return HY_EINVAL;
+    }
+    if (!p->keys.count(g) && p->keys.size() >= 4 * HY_MAX_GALOIS) {
+      cudaFree(tmp);
+      hy_set_error("too many keys");
+      return HY_EINVAL;
+    }
+    const u64* src = keys + (size_t)e * key_words;
+    cudaError_t ce = cudaMemcpy(tmp, src, key_words * sizeof(u64),
+                                keys_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) {
+      cudaFree(tmp);
+      hy_set_error("key copy: %s", cudaGetErrorString(ce));
+      return HY_ECUDA;
+    }
+    KeyEntry& ke = p->keys[g];
+    ke.g = g;
+    if (!ke.ntt) {
+      ce = cudaMalloc(&ke.ntt, 2 * key_words * sizeof(u64));
+      if (ce != cudaSuccess) {
+        p->keys.erase(g);
+        cudaFree(tmp);
+        hy_set_error("key alloc: %s", cudaGetErrorString(ce));
+        return HY_ENOMEM;
+      }
+    }
+    hy_status st = hyk::key_to_ntt(p, tmp, ke.ntt, 0);
+    if (st != HY_OK) {
+      cudaFree(tmp);
+      return st;
+    }
+  }
+  cudaError_t ce = cudaDeviceSynchronize();
+  cudaFree(tmp);
+  p->keys_version++;
+  HY_CHECK(ce == cudaSuccess, HY_ECUDA, "key upload: %s", cudaGetErrorString(ce));
+  return HY_OK;
+}
+
+// ============================================================================================
+// weights
+// ============================================================================================
+extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, const int8_t* Wt, hy_weights** out) {
+  HY_CHECK(p && sh && Wt && out, HY_EINVAL, "null argument");
+  hy_layout lay;
+  HY_TRY(hy_plan_layout(p->N, p->t, sh, &lay));
+  lay.L = p->L;
+  HY_CUDA_TRY(cudaSetDevice(p->device));
+  hy_weights* w = new hy_weights();
+  memset((void*)w, 0, sizeof(*w));
+  w->p = p;
+  w->shape = *sh;
+  w->lay = lay;
+  const int T = (int)lay.n_taps;
+  const bool dw = sh->depthwise != 0;
+  if (dw) {
+    w->M = lay.cn == 2 ? 2 : 1;
+    w->K = T;
+    w->wblocks = (int)lay.Jc;
+  } else {
+    w->M = lay.cn == 2 ? (int)(4 * lay.Jo) : (int)lay.Jo;
+    w->K = (int)lay.Jc * T;
+    w->wblocks = 1;
+  }
+  const int tm = w->M >= 16 ? 16 : (w->M >= 8 ? 8 : (w->M >= 4 ? 4 : (w->M >= 2 ? 2 : 1)));
+  const int Mpad = (w->M + tm - 1) / tm * tm;
+  // weight tables (S0): row layout documented in DESIGN.md
+  std::vector<int32_t> wm((size_t)w->wblocks * Mpad * w->K, 0);
+  const uint32_t Ci = sh->Ci, Co = dw ? sh->Ci : sh->Co, kw = sh->kw;
+  auto Wat = [&](uint32_t o, uint32_t c, int tau) -> int32_t {
+    const uint32_t dy = tau / kw, dx = tau % kw;
+    if (dw) return (o == c && c < Ci) ? Wt[((size_t)c * sh->kh + dy) * kw + dx] : 0;
+    if (o >= Co || c >= Ci) return 0;
+    return Wt[(((size_t)o * Ci + c) * sh->kh + dy) * kw + dx];
+  };
+  for (int b = 0; b < w->wblocks; b++)
+    for (int row = 0; row < w->M; row++)
+      for (int kk = 0; kk < w->K; kk++) {
+        int32_t v;
+        if (dw) {
+          v = lay.cn == 2 ? Wat(2 * b + row, 2 * b + row, kk) : Wat(b, b, kk);
+        } else if (lay.cn == 2) {
+          // row = (g*2 + d)*2 + c : slot row c of diagonal d pairs input 2j+c with output 2g+(c^d)
+          const int g = row / 4, d = (row / 2) % 2, c = row % 2;
+          const int j = kk / T, tau = kk % T;
+          v = Wat(2 * g + (c ^ d), 2 * j + c, tau);
+        } else {
+          v = Wat(row, kk / T, kk % T);
+        }
+        wm[((size_t)b * Mpad + row) * w->K + kk] = v;
+      }
+  hy_status st = upload((void**)&w->d_wm, wm.data(), wm.size() * sizeof(int32_t));
+  if (st != HY_OK) {
+    hy_weights_destroy(w);
+    return st;
+  }
+  const size_t L = p->L, N = p->N, ctw = 2 * L * N;
+  const size_t Jin = (size_t)lay.U * lay.Jc, Jo = (size_t)lay.U * lay.Jo;
+  // sign plaintext [k,-k]: [k h]_t at X^{N/4}, X^{3N/4}, centered lift (R14)
+  if (lay.cn == 2) {
+    std::vector<u64> sp(L * N, 0);
+    for (size_t l = 0; l < L; l++) {
+      const int64_t sc = lay.sign_coeff;
+      const u64 v = sc >= 0 ? (u64)sc % p->q[l] : p->q[l] - ((u64)(-sc) % p->q[l]);
+      sp[l * N + N / 4] = v;
+      sp[l * N + 3 * N / 4] = v;
+    }
+    u64* tmp = nullptr;
+    if ((st = upload((void**)&tmp, sp.data(), sp.size() * sizeof(u64))) != HY_OK) {
+      hy_weights_destroy(w);
+      return st;
+    }
+    cudaMalloc(&w->d_sign, 2 * L * N * sizeof(u64));
+    st = hyk::ntt_poly_fwd(p, tmp, w->d_sign, 1, 0);
+    if (st == HY_OK) st = hyk::shoup_table(p, w->d_sign, w->d_sign + L * N, 1, 0);
+    cudaDeviceSynchronize();
+    cudaFree(tmp);
+    if (st != HY_OK) {
+      hy_weights_destroy(w);
+      return st;
+    }
+  }
+  // workspace
+  struct A {
+    u64** ptr;
+    size_t words;
+  } allocs[] = {
+      {&w->d_D, Jin * L * L * N},
+      {&w->d_C0, Jin * L * N},
+      {&w->d_R, Jin * T * ctw},
+      {&w->d_P, Jo * ctw * ((lay.cn == 2 && !dw) ? 2 : 1)},
+      {&w->d_D2, (lay.cn == 2 && !dw) ? Jo * L * L * N + Jo * L * N : 0},
+      {&w->d_in, Jin * ctw},
+      {&w->d_out, Jo * ctw},
+  };
+  for (auto& a : allocs) {
+    if (!a.words) continue;
+    cudaError_t ce = cudaMalloc(a.ptr, a.words * sizeof(u64));
+    if (ce != cudaSuccess) {
+      hy_weights_destroy(w);
+      hy_set_error("workspace allocation of %zu MiB failed: %s", a.words * 8 >> 20, cudaGetErrorString(ce));
+      return HY_ENOMEM;
+    }
+  }
+  HY_CUDA_TRY(cudaMalloc(&w->d_tap_keys, T * sizeof(u64*)));
+  HY_CUDA_TRY(cudaMalloc(&w->d_tap_g, T * sizeof(uint32_t)));
+  w->keys_version = ~0ull;
+  HY_CUDA_TRY(cudaDeviceSynchronize());
+  *out = w;
+  return HY_OK;
+}
+
+extern "C" hy_status hy_weights_set_stage_events(hy_weights* w, void* const* events, uint32_t n) {
+  HY_CHECK(w && (n == 0 || events) && n <= 5, HY_EINVAL, "bad stage events");
+  for (uint32_t i = 0; i < n; i++) w->ev[i] = (cudaEvent_t)events[i];
+  w->n_ev = n;
+  return HY_OK;
+}
+
+extern "C" hy_status hy_weights_layout(const hy_weights* w, hy_layout* out) {
+  HY_CHECK(w && out, HY_EINVAL, "null argument");
+  *out = w->lay;
+  return HY_OK;
+}
+
+extern "C" void hy_weights_destroy(hy_weights* w) {
+  if (!w) return;
+  cudaSetDevice(w->p->device);
+  cudaFree(w->d_wm);
+  cudaFree(w->d_sign);
+  cudaFree(w->d_D);
+  cudaFree(w->d_C0);
+  cudaFree(w->d_R);
+  cudaFree(w->d_P);
+  cudaFree(w->d_D2);
+  cudaFree(w->d_in);
+  cudaFree(w->d_out);
+  cudaFree(w->d_tap_keys);
+  cudaFree(w->d_tap_g);
+  delete w;
+}
+
+static hy_status bind_keys(hy_weights* w) {
+  hy_params* p = w->p;
+  if (w->keys_version == p->keys_version) return HY_OK;
+  const hy_layout& lay = w->lay;
+  const uint32_t row = p->N / 2;
+  std::vector<u64*> ptrs(lay.n_taps, nullptr);
+  std::vector<uint32_t> gs(lay.n_taps, 1);
+  for (uint32_t tau = 0; tau < lay.n_taps; tau++) {
+    const int64_t st = (((int64_t)lay.tap_step[tau] % (int64_t)row) + row) % row;
+    if (st == 0) continue;
+    const uint32_t g = (uint32_t)powmod(3, (u64)st, 2 * (u64)p->N);
+    auto it = p->keys.find(g);
+    HY_CHECK(it != p->keys.end(), HY_ENOKEY, "no Galois key for element %u (tap %u, step %d)", g, tau,
+             lay.tap_step[tau]);
+    ptrs[tau] = it->second.ntt;
+    gs[tau] = g;
+  }
+  w->d_swap_key = nullptr;
+  if (lay.cn == 2 && !w->shape.depthwise) {
+    auto it = p->keys.find(2 * p->N - 1);
+    HY_CHECK(it != p->keys.end(), HY_ENOKEY, "no Galois key for the row swap (element %u)", 2 * p->N - 1);
+    w->d_swap_key = it->second.ntt;
+  }
+  HY_CUDA_TRY(cudaMemcpy(w->d_tap_keys, ptrs.data(), ptrs.size() * sizeof(u64*), cudaMemcpyHostToDevice));
+  HY_CUDA_TRY(cudaMemcpy(w->d_tap_g, gs.data(), gs.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  w->keys_version = p->keys_version;
+  return HY_OK;
+}
+
+// ============================================================================================
+// evaluation
+// ============================================================================================
+extern "C" hy_status hy_conv_eval(hy_weights* w, const uint64_t* ct_in, size_t J, uint64_t* ct_out, size_t Jout,
+                                  void* stream) {
+  HY_CHECK(w && ct_in && ct_out, HY_EINVAL, "null argument");
+  const hy_layout& lay = w->lay;
+  HY_CHECK(J > 0 && J % lay.Jc == 0, HY_ESHAPE, "J=%zu is not a positive multiple of Jc=%u", J, lay.Jc);
+  const size_t nu = J / lay.Jc;
+  HY_CHECK(nu <= lay.U, HY_ESHAPE, "J=%zu covers %zu units > U=%u", J, nu, lay.U);
+  HY_CHECK(Jout == nu * lay.Jo, HY_ESHAPE, "Jout=%zu, expected %zu", Jout, nu * lay.Jo);
+  hy_params* p = w->p;
+  HY_CUDA_TRY(cudaSetDevice(p->device));
+  HY_TRY(bind_keys(w));
+  cudaStream_t s = (cudaStream_t)stream;
+  auto mark = [&](uint32_t i) -> hy_status {
+    if (i < w->n_ev) HY_CUDA_TRY(cudaEventRecord(w->ev[i], s));
+    return HY_OK;
+  };
+  HY_TRY(mark(0));
+  HY_TRY(hyk::permdecomp(p, ct_in, J, w->d_D, w->d_C0, s));  // S1 PermDecomp
+  HY_TRY(mark(1));
+  HY_TRY(hyk::permauto(p, w->d_D, w->d_C0, J, (int)lay.n_taps, w->d_tap_keys, w->d_tap_g, w->d_R, s));  // S2
+  HY_TRY(mark(2));
+  HY_TRY(hyk::mac(w, nu, s));  // S3 lazy MAC + WHT + reduce + sign PMult
+  HY_TRY(mark(3));
+  HY_TRY(hyk::finish_outputs(w, nu, ct_out, s));  // S4 alignment + S5 INTT
+  HY_TRY(mark(4));
+  return HY_OK;
+}
+
+extern "C" hy_status hy_conv_eval_host(hy_weights* w, const uint64_t* in, size_t J, uint64_t* out, size_t Jout,
+                                       void* stream) {
+  HY_CHECK(w && in && out, HY_EINVAL, "null argument");
+  const size_t ctw = 2 * (size_t)w->p->L * w->p->N;
+  HY_CHECK(J <= (size_t)w->lay.U * w->lay.Jc && Jout <= (size_t)w->lay.U * w->lay.Jo, HY_ESHAPE, "too many cts");
+  HY_CUDA_TRY(cudaSetDevice(w->p->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  HY_CUDA_TRY(cudaMemcpyAsync(w->d_in, in, J * ctw * sizeof(u64), cudaMemcpyHostToDevice, s));
+  HY_TRY(hy_conv_eval(w, w->d_in, J, w->d_out, Jout, stream));
+  HY_CUDA_TRY(cudaMemcpyAsync(out, w->d_out, Jout * ctw * sizeof(u64), cudaMemcpyDeviceToHost, s));
+  HY_CUDA_TRY(cudaStreamSynchronize(s));
+  return HY_OK;
+}
+
+// ============================================================================================
+// per-stage entry points
+// ============================================================================================
+extern "C" hy_status hy_poly_mul(const hy_params* p, const uint64_t* a, const uint64_t* b, uint64_t* c, size_t n,
+                                 void* stream) {
+  HY_CHECK(p && a && b && c, HY_EINVAL, "null argument");
+  if (n == 0) return HY_OK;
+  HY_CUDA_TRY(cudaSetDevice(p->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t words = n * p->L * p->N;
+  u64* tmp = nullptr;
+  HY_CUDA_TRY(cudaMalloc(&tmp, 2 * words * sizeof(u64)));
+  hy_status st = hyk::ntt_poly_fwd(p, a, tmp, n, s);
+  if (st == HY_OK) st = hyk::ntt_poly_fwd(p, b, tmp + words, n, s);
+  if (st == HY_OK) st = hyk::pointwise_mul(p, tmp, tmp + words, c, n, s);
+  cudaError_t ce = cudaStreamSynchronize(s);
+  cudaFree(tmp);
+  if (st != HY_OK) return st;
+  HY_CHECK(ce == cudaSuccess, HY_ECUDA, "%s", cudaGetErrorString(ce));
+  return HY_OK;
+}
+
+extern "C" hy_status hy_ntt_roundtrip(const hy_params* p, uint64_t* x, size_t n, void* stream) {
+  HY_CHECK(p && x, HY_EINVAL, "null argument");
+  if (n == 0) return HY_OK;
+  HY_CUDA_TRY(cudaSetDevice(p->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  HY_TRY(hyk::ntt_poly_fwd(p, x, x, n, s));
+  HY_TRY(hyk::ntt_poly_inv(p, x, x, n, s));
+  return HY_OK;
+}
+
+extern "C" hy_status hy_rotate(hy_params* p, const uint64_t* ct_in, uint32_t g, uint64_t* ct_out, size_t n,
+                               void* stream) {
+  HY_CHECK(p && ct_in && ct_out, HY_EINVAL, "null argument");
+  if (n == 0) return HY_OK;
+  auto it = p->keys.find(g);
+  HY_CHECK(it != p->keys.end(), HY_ENOKEY, "no Galois key for element %u", g);
+  HY_CUDA_TRY(cudaSetDevice(p->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  u64* work = nullptr;
+  HY_CUDA_TRY(cudaMalloc(&work, n * (p->L * p->L + p->L) * p->N * sizeof(u64)));
+  hy_status st = hyk::rotate_ct(p, ct_in, g, it->second.ntt, ct_out, n, work, s);
+  cudaError_t ce = cudaStreamSynchronize(s);
+  cudaFree(work);
+  if (st != HY_OK) return st;
+  HY_CHECK(ce == cudaSuccess, HY_ECUDA, "%s", cudaGetErrorString(ce));
+  return HY_OK;
+}
+
+// ============================================================================================
+// debug decryption
+// ============================================================================================
+namespace {
+// minimal unsigned big integer (little-endian 32-bit limbs) for the exact CRT rounding
+struct Big {
+  std::vector<uint32_t> d;
+  void trim() {
+    while (!d.empty() && d.back() == 0) d.pop_back();
+  }
+  static Big from(u64 x) {
+    Big b;
+    b.d = {(uint32_t)x, (uint32_t)(x >> 32)};
+    b.trim();
+    return b;
+  }
+  Big mul(u64 m) const {
+    Big r;
+    const uint32_t m0 = (uint32_t)m, m1 = (uint32_t)(m >> 32);
+    r.d.assign(d.size() + 3, 0);
+    for (int pass = 0; pass < 2; pass++) {
+      const u64 mm = pass ? m1 : m0;
+      u64 carry = 0;
+      size_t i = 0;
+      for (; i < d.size(); i++) {
+        u64 cur = (u64)r.d[i + pass] + (u64)d[i] * mm + carry;
+        r.d[i + pass] = (uint32_t)cur;
+        carry = cur >> 32;
+      }
+      for (size_t k = i + pass; carry; k++) {
+        u64 cur = (u64)r.d[k] + carry;
+        r.d[k] = (uint32_t)cur;
+        carry = cur >> 32;
+      }
+    }
+    r.trim();
+    return r;
+  }
+  Big add(const Big& o) const {
+    Big r;
+    r.d.assign(std::max(d.size(), o.d.size()) + 1, 0);
+    u64 carry = 0;
+    for (size_t i = 0; i < r.d.size(); i++) {
+      u64 cur = carry + (i < d.size() ? d[i] : 0) + (i < o.d.size() ? o.d[i] : 0);
+      r.d[i] = (uint32_t)cur;
+      carry = cur >> 32;
+    }
+    r.trim();
+    return r;
+  }
+  Big sub(const Big& o) const {  // requires *this >= o
+    Big r = *this;
+    int64_t borrow = 0;
+    for (size_t i = 0; i < r.d.size(); i++) {
+      int64_t cur = (int64_t)r.d[i] - (i < o.d.size() ? o.d[i] : 0) - borrow;
+      borrow = cur < 0;
+      r.d[i] = (uint32_t)(cur + (borrow ? (1ll << 32) : 0));
+    }
+    r.trim();
+    return r;
+  }
+  int cmp(const Big& o) const {
+    if (d.size() != o.d.size()) return d.size() < o.d.size() ? -1 : 1;
+    for (size_t i = d.size(); i-- > 0;)
+      if (d[i] != o.d[i]) return d[i] < o.d[i] ? -1 : 1;
+    return 0;
+  }
+};
+
+// host negacyclic NTT mod t (t < 2^32): out[k] = m(zeta^{2 bitrev(k) + 1})
+void host_ntt_t(std::vector<u64>& a, u64 t, u64 zeta, uint32_t logN) {
+  const uint32_t N = 1u << logN;
+  std::vector<u64> zr(N);
+  for (uint32_t k = 0; k < N; k++) zr[k] = powmod(zeta, bitrev(k, logN), t);
+  for (uint32_t m = 1, tt = N / 2; m < N; m *= 2, tt /= 2)
+    for (uint32_t i = 0; i < m; i++) {
+      const u64 w = zr[m + i];
+      for (uint32_t j = 2 * i * tt; j < 2 * i * tt + tt; j++) {
+        const u64 U = a[j], V = a[j + tt] * w % t;
+        a[j] = (U + V) % t;
+        a[j + tt] = (U + t - V) % t;
+      }
+    }
+}
+}  // namespace
+
+extern "C" hy_status hy_decrypt_debug(const hy_params* p, const int8_t* sk, const uint64_t* ct, size_t n,
+                                      uint32_t scale, uint64_t* slots_out) {
+  HY_CHECK(p && sk && ct && slots_out, HY_EINVAL, "null argument");
+  HY_CHECK(scale % p->t != 0, HY_EINVAL, "scale must be invertible mod t");
+  if (n == 0) return HY_OK;
+  HY_CUDA_TRY(cudaSetDevice(p->device));
+  const size_t L = p->L, N = p->N;
+  std::vector<u64> s_res(L * N);
+  for (size_t l = 0; l < L; l++)
+    for (size_t k = 0; k < N; k++) {
+      const int v = sk[k];
+      HY_CHECK(v >= -1 && v <= 1, HY_EINVAL, "secret key must be ternary");
+      s_res[l * N + k] = v >= 0 ? (u64)v : p->q[l] - 1;
+    }
+  u64 *d_s = nullptr, *d_sn = nullptr, *d_x = nullptr, *d_work = nullptr;
+  HY_CUDA_TRY(cudaMalloc(&d_s, L * N * 8));
+  HY_CUDA_TRY(cudaMalloc(&d_sn, 2 * L * N * 8));
+  HY_CUDA_TRY(cudaMalloc(&d_x, n * L * N * 8));
+  HY_CUDA_TRY(cudaMalloc(&d_work, n * L * N * 8));
+  HY_CUDA_TRY(cudaMemcpy(d_s, s_res.data(), L * N * 8, cudaMemcpyHostToDevice));
+  hy_status st = hyk::ntt_poly_fwd(p, d_s, d_sn, 1, 0);
+  if (st == HY_OK) st = hyk::shoup_table(p, d_sn, d_sn + L * N, 1, 0);
+  if (st == HY_OK) st = hyk::decrypt_phase(p, d_sn, d_sn + L * N, ct, n, d_x, d_work, 0);
+  std::vector<u64> x(n * L * N);
+  cudaError_t ce = cudaMemcpy(x.data(), d_x, n * L * N * 8, cudaMemcpyDeviceToHost);
+  cudaFree(d_s);
+  cudaFree(d_sn);
+  cudaFree(d_x);
+  cudaFree(d_work);
+  if (st != HY_OK) return st;
+  HY_CHECK(ce == cudaSuccess, HY_ECUDA, "%s", cudaGetErrorString(ce));
+  // exact CRT rounding: m = round(sum_l t z_l / q_l) mod t, z_l = x_l [(Q/q_l)^{-1}]_{q_l}
+  const u64 t = p->t;
+  Big Q = Big::from(1);
+  for (size_t l = 0; l < L; l++) Q = Q.mul(p->q[l]);
+  std::vector<Big> Ql(L);
+  std::vector<u64> inv(L);
+  for (size_t l = 0; l < L; l++) {
+    Big b = Big::from(1);
+    u64 r = 1;
+    for (size_t m = 0; m < L; m++)
+      if (m != l) {
+        b = b.mul(p->q[m]);
+        r = mulmod(r, p->q[m] % p->q[l], p->q[l]);
+      }
+    Ql[l] = b;
+    inv[l] = invmod(r, p->q[l]);
+  }
+  const Big Q2 = Q.mul(2);
+  const u64 sinv = invmod(scale % t, t);
+  std::vector<u64> m(N);
+  const uint32_t half = (uint32_t)N / 2;
+  for (size_t o = 0; o < n; o++) {
+    for (size_t k = 0; k < N; k++) {
+      u64 isum = 0;
+      Big S;
+      for (size_t l = 0; l < L; l++) {
+        const u64 z = mulmod(x[(o * L + l) * N + k], inv[l], p->q[l]);
+        const u128 tz = (u128)t * z;
+        isum += (u64)(tz / p->q[l]);
+        S = S.add(Ql[l].mul((u64)(tz % p->q[l])));
+      }
+      Big X = S.mul(2).add(Q);  // round(S/Q) = floor((2S + Q) / 2Q)
+      u64 j = 0;
+      while (X.cmp(Q2) >= 0) {
+        X = X.sub(Q2);
+        j++;
+      }
+      m[k] = (isum + j) % t;
+    }
+    host_ntt_t(m, t, p->zeta_t, p->logN);
+    for (uint32_t r = 0; r < 2; r++)
+      for (uint32_t i = 0; i < half; i++) {
+        u64 e = powmod(3, i, 2 * (u64)N);
+        if (r) e = 2 * (u64)N - e;
+        const uint32_t kk = bitrev((uint32_t)((e - 1) / 2), p->logN);
+        slots_out[o * N + r * half + i] = mulmod(m[kk], sinv, t);
+      }
+  }
+  return HY_OK;
+}

@@ -1,0 +1,162 @@
+// Internal definitions shared by the library's translation units (NOT shared with oracle/).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/hyena.h"
+
+typedef uint64_t u64;
+typedef unsigned __int128 u128;
+
+// ------------------------------------------------------------------------------------
+// error plumbing
+// ------------------------------------------------------------------------------------
+void hy_set_error(const char* fmt, ...);
+
+#define HY_CUDA_TRY(expr)                                                                     \
+  do {                                                                                        \
+    cudaError_t _e = (expr);                                                                  \
+    if (_e != cudaSuccess) {                                                                  \
+      hy_set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e));        \
+      return HY_ECUDA;                                                                        \
+    }                                                                                         \
+  } while (0)
+
+void hy_count_launch();
+
+#define HY_LAUNCH_CHECK()                                                                     \
+  do {                                                                                        \
+    hy_count_launch();                                                                        \
+    cudaError_t _e = cudaGetLastError();                                                      \
+    if (_e != cudaSuccess) {                                                                  \
+      hy_set_error("%s:%d kernel launch: %s", __FILE__, __LINE__, cudaGetErrorString(_e));    \
+      return HY_ECUDA;                                                                        \
+    }                                                                                         \
+  } while (0)
+
+#define HY_TRY(expr)                 \
+  do {                               \
+    hy_status _s = (expr);           \
+    if (_s != HY_OK) return _s;      \
+  } while (0)
+
+// ------------------------------------------------------------------------------------
+// per-limb constants passed to kernels by value
+// ------------------------------------------------------------------------------------
+struct LimbConst {
+  u64 q;
+  u64 two_q;
+  u64 ninv, ninv_sh;      // N^{-1} mod q and its Shoup companion
+  u64 one_sh;             // floor(2^64 / q): Shoup companion of 1
+  u64 c30, c30_sh;        // 2^30 mod q and Shoup companion
+  u64 off;                // q * ceil(2^59 / q): makes |x| < 2^59 signed values nonnegative
+};
+
+struct DevTables {
+  // [L][N] each, device
+  u64* psi_rev;       // psi^{bitrev(k)}
+  u64* psi_rev_sh;
+  u64* ipsi_rev;      // psi^{-bitrev(k)}
+  u64* ipsi_rev_sh;
+};
+
+struct KeyEntry {
+  uint32_t g;
+  u64* ntt;  // device [L digits][2][L limbs][N] values, then the same again for Shoup companions
+};
+
+struct hy_params {
+  uint32_t N, logN, L;
+  u64 t;
+  u64 q[HY_MAX_LIMBS];
+  int device;
+  LimbConst lc[HY_MAX_LIMBS];
+  DevTables tab;
+  u64* d_scratch = nullptr;  // small scratch
+  // plaintext side (host)
+  u64 zeta_t;
+  std::map<uint32_t, KeyEntry> keys;
+  u64 keys_version = 0;  // bumped by every hy_keys_upload
+};
+
+struct hy_weights {
+  hy_params* p;
+  hy_conv_shape shape;
+  hy_layout lay;
+  int M;            // MAC rows per unit
+  int K;            // MAC depth per unit (Jc*T dense; T depthwise)
+  int wblocks;      // number of distinct weight blocks (1 dense, Jc depthwise)
+  int32_t* d_wm;    // [wblocks][M][K]
+  u64* d_sign;      // [L][N] NTT form of the [k,-k] plaintext, then [L][N] Shoup companions
+  // workspace (device)
+  u64* d_D;         // [U*Jc][L digit][L limb][N] NTT-form digits
+  u64* d_C0;        // [U*Jc][L][N]    NTT(c0)
+  u64* d_R;         // [U*Jc][T][2][L][N] rotated inputs (NTT form)
+  u64* d_P;         // [U*Jo][cn'][2][L][N] partial sums (NTT form)
+  u64* d_D2;        // [U*Jo][L][L][N] digits of P_{g,1}.c1 for the row swap
+  u64* d_in;        // staging for hy_conv_eval_host
+  u64* d_out;
+  u64** d_tap_keys;            // device array of key pointers per tap (nullptr = identity)
+  uint32_t* d_tap_g;           // device array of Galois elements per tap
+  u64* d_swap_key;
+  u64 keys_version;            // params->keys_version the tap table was built from
+  cudaEvent_t ev[5];           // optional stage-boundary events (bench)
+  uint32_t n_ev;
+};
+
+// ------------------------------------------------------------------------------------
+// device modular arithmetic
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ u64 shoup_mul(u64 x, u64 w, u64 w_sh, u64 q) {
+  // x * w mod q in [0, 2q) for any 64-bit x (Shoup; w < q, w_sh = floor(w 2^64 / q)).
+  u64 hi = __umul64hi(x, w_sh);
+  return x * w - hi * q;
+}
+
+__device__ __forceinline__ u64 csub(u64 x, u64 m) { return x >= m ? x - m : x; }
+
+// x in [0, 2^64): x mod q in [0, 2q)  (Shoup with w = 1)
+__device__ __forceinline__ u64 reduce_2q(u64 x, u64 one_sh, u64 q) { return x - __umul64hi(x, one_sh) * q; }
+
+// full 64x64 -> mod q, both operands < 2^64 and w arbitrary (no precomputation): slow path.
+__device__ __forceinline__ u64 mulmod_slow(u64 a, u64 b, u64 q) {
+  u128 p = (u128)a * b;
+  return (u64)(p % q);
+}
+
+// ------------------------------------------------------------------------------------
+// host helpers (library-internal)
+// ------------------------------------------------------------------------------------
+namespace hyhost {
+u64 mulmod(u64 a, u64 b, u64 m);
+u64 powmod(u64 a, u64 e, u64 m);
+u64 invmod(u64 a, u64 m);
+bool is_prime(u64 n);
+u64 shoup(u64 w, u64 q);
+uint32_t bitrev(uint32_t x, uint32_t bits);
+}  // namespace hyhost
+
+// kernels API (internal)
+namespace hyk {
+// forward NTT of n jobs; job table decides sources
+hy_status ntt_poly_fwd(const hy_params* p, const u64* src, u64* dst, size_t npoly, cudaStream_t s);  // [n][L][N]
+hy_status ntt_poly_inv(const hy_params* p, const u64* src, u64* dst, size_t npoly, cudaStream_t s);  // [n][L][N]
+hy_status pointwise_mul(const hy_params* p, const u64* a, const u64* b, u64* c, size_t npoly, cudaStream_t s);
+hy_status shoup_table(const hy_params* p, const u64* w, u64* w_sh, size_t npoly, cudaStream_t s);  // [n][L][N]
+hy_status key_to_ntt(const hy_params* p, const u64* key_coeff, u64* key_ntt, cudaStream_t s);
+hy_status permdecomp(const hy_params* p, const u64* ct, size_t nct, u64* D, u64* C0, cudaStream_t s);
+hy_status permauto(const hy_params* p, const u64* D, const u64* C0, size_t nct, int ntap, u64* const* d_tap_keys,
+                   const uint32_t* h_galois_per_tap, u64* R, cudaStream_t s);
+hy_status mac(const hy_weights* w, size_t nunits, cudaStream_t s);
+hy_status rowswap_digits(const hy_params* p, const u64* Pd, size_t nout, u64* D2, cudaStream_t s);
+hy_status finish_outputs(const hy_weights* w, size_t nunits, u64* ct_out, cudaStream_t s);
+hy_status rotate_ct(const hy_params* p, const u64* ct_in, uint32_t g, const u64* key, u64* ct_out, size_t n,
+                    u64* work, cudaStream_t s);
+hy_status decrypt_phase(const hy_params* p, const u64* s_ntt, const u64* s_ntt_sh, const u64* ct, size_t n,
+                        u64* x_out, u64* work, cudaStream_t st);
+}  // namespace hyk

@@ -1,0 +1,229 @@
+"""ctypes binding for libhyena.so (include/hyena.h).  Argument marshalling only: every step of
+the encrypted convolution runs in the library's CUDA kernels; nothing here computes.
+
+Device buffers are passed as torch CUDA tensors (dtype torch.uint64, contiguous); host buffers
+as numpy arrays.  Every failing call raises HyenaError with hy_last_error()'s message.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import numpy as np
+
+__all__ = ["HyenaError", "hy_conv_shape", "hy_layout", "load_library", "library_path", "hy_last_error",
+           "hy_plan_layout", "hy_params_create", "hy_params_destroy", "hy_keys_upload", "hy_encode_weights",
+           "hy_weights_layout", "hy_weights_destroy", "hy_conv_eval", "hy_conv_eval_host", "hy_poly_mul",
+           "hy_ntt_roundtrip", "hy_rotate", "hy_decrypt_debug", "hy_kernel_launches", "hy_weights_set_stage_events",
+           "layout_dict", "EXPORTED"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+HY_MAX_TAPS = 49
+HY_MAX_GALOIS = 64
+
+# every symbol include/hyena.h declares
+EXPORTED = ["hy_last_error", "hy_plan_layout", "hy_params_create", "hy_params_destroy", "hy_keys_upload",
+            "hy_encode_weights", "hy_weights_layout", "hy_weights_destroy", "hy_conv_eval", "hy_conv_eval_host",
+            "hy_poly_mul", "hy_ntt_roundtrip", "hy_rotate", "hy_decrypt_debug", "hy_kernel_launches",
+            "hy_weights_set_stage_events"]
+
+
+class HyenaError(RuntimeError):
+    pass
+
+
+class hy_conv_shape(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint32) for n in ("Ci", "Co", "H", "W", "kh", "kw", "pad", "stride", "depthwise",
+                                                "batch")] + [("k", ctypes.c_int32), ("force_cn", ctypes.c_int32)]
+
+
+class hy_layout(ctypes.Structure):
+    _fields_ = ([(n, ctypes.c_uint32) for n in ("N", "L", "Hout", "Wout", "Wp", "Hp", "mode", "per_row", "Hb", "Hv",
+                                                 "bands", "G", "cn", "U", "Jc", "Jo", "J", "Jout", "n_taps")]
+                + [("tap_dy", ctypes.c_int32 * HY_MAX_TAPS), ("tap_dx", ctypes.c_int32 * HY_MAX_TAPS),
+                   ("tap_step", ctypes.c_int32 * HY_MAX_TAPS)]
+                + [(n, ctypes.c_uint32) for n in ("k", "scale", "h")]
+                + [("sign_coeff", ctypes.c_int32), ("n_galois", ctypes.c_uint32),
+                   ("galois", ctypes.c_uint32 * HY_MAX_GALOIS)])
+
+
+def layout_dict(lay: hy_layout) -> dict:
+    d = {n: getattr(lay, n) for n, _ in hy_layout._fields_ if n not in ("tap_dy", "tap_dx", "tap_step", "galois")}
+    d["tap_step"] = list(lay.tap_step[:lay.n_taps])
+    d["galois"] = list(lay.galois[:lay.n_galois])
+    return d
+
+
+_lib = None
+
+
+def library_path() -> str:
+    return os.path.join(_HERE, "libhyena.so")
+
+
+def load_library() -> ctypes.CDLL:
+    """Load the in-tree libhyena.so (built by __graft_entry__.build()); raises if missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = library_path()
+    if not os.path.exists(path):
+        raise HyenaError(f"{path} not built: run `python -m paper_2311_12519_b200.build` (no CPU fallback exists)")
+    lib = ctypes.CDLL(path)
+    vp, u32, u64, i32, sz = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_size_t
+    sig = {
+        "hy_last_error": (ctypes.c_char_p, []),
+        "hy_plan_layout": (i32, [u32, u64, ctypes.POINTER(hy_conv_shape), ctypes.POINTER(hy_layout)]),
+        "hy_params_create": (i32, [u32, vp, u32, u64, ctypes.c_int, ctypes.POINTER(vp)]),
+        "hy_params_destroy": (None, [vp]),
+        "hy_keys_upload": (i32, [vp, u32, vp, vp, ctypes.c_int]),
+        "hy_encode_weights": (i32, [vp, ctypes.POINTER(hy_conv_shape), vp, ctypes.POINTER(vp)]),
+        "hy_weights_layout": (i32, [vp, ctypes.POINTER(hy_layout)]),
+        "hy_weights_destroy": (None, [vp]),
+        "hy_conv_eval": (i32, [vp, vp, sz, vp, sz, vp]),
+        "hy_conv_eval_host": (i32, [vp, vp, sz, vp, sz, vp]),
+        "hy_poly_mul": (i32, [vp, vp, vp, vp, sz, vp]),
+        "hy_ntt_roundtrip": (i32, [vp, vp, sz, vp]),
+        "hy_rotate": (i32, [vp, vp, u32, vp, sz, vp]),
+        "hy_decrypt_debug": (i32, [vp, vp, vp, sz, u32, vp]),
+        "hy_kernel_launches": (u64, []),
+        "hy_weights_set_stage_events": (i32, [vp, vp, u32]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def hy_last_error() -> str:
+    return load_library().hy_last_error().decode()
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        raise HyenaError(f"{what} failed ({status}): {hy_last_error()}")
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return int(stream)
+
+
+def _dev_ptr(t, words: Optional[int] = None) -> int:
+    """data_ptr of a contiguous CUDA uint64 tensor (checked)."""
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.uint64 and t.is_contiguous()):
+        raise HyenaError("expected a contiguous CUDA torch.uint64 tensor")
+    if words is not None and t.numel() < words:
+        raise HyenaError(f"tensor has {t.numel()} words, need {words}")
+    return t.data_ptr()
+
+
+def _shape(**kw) -> hy_conv_shape:
+    s = hy_conv_shape()
+    for k, v in kw.items():
+        setattr(s, k, int(v))
+    if "stride" not in kw:
+        s.stride = 1
+    return s
+
+
+def hy_plan_layout(N: int, t: int, **shape) -> hy_layout:
+    lay = hy_layout()
+    s = _shape(**shape)
+    _check(load_library().hy_plan_layout(N, t, ctypes.byref(s), ctypes.byref(lay)), "hy_plan_layout")
+    return lay
+
+
+def hy_params_create(N: int, primes: Sequence[int], t: int, device: int = 0) -> int:
+    q = (ctypes.c_uint64 * len(primes))(*[int(x) for x in primes])
+    out = ctypes.c_void_p()
+    _check(load_library().hy_params_create(N, q, len(primes), t, device, ctypes.byref(out)), "hy_params_create")
+    return out.value
+
+
+def hy_params_destroy(p: int):
+    load_library().hy_params_destroy(p)
+
+
+def hy_keys_upload(p: int, galois_elts: Sequence[int], keys):
+    """keys: numpy uint64 [n][L][2][L][N] (host) or CUDA uint64 tensor of the same shape."""
+    g = (ctypes.c_uint32 * len(galois_elts))(*[int(x) for x in galois_elts])
+    if isinstance(keys, np.ndarray):
+        k = np.ascontiguousarray(keys, dtype=np.uint64)
+        _check(load_library().hy_keys_upload(p, len(galois_elts), g, k.ctypes.data, 0), "hy_keys_upload")
+    else:
+        _check(load_library().hy_keys_upload(p, len(galois_elts), g, _dev_ptr(keys), 1), "hy_keys_upload")
+
+
+def hy_encode_weights(p: int, weights: np.ndarray, **shape) -> int:
+    """weights: int8 [Co][Ci][kh][kw] (or [C][kh][kw] depthwise); shape: hy_conv_shape fields."""
+    Wc = np.ascontiguousarray(weights, dtype=np.int8)
+    s = _shape(**shape)
+    out = ctypes.c_void_p()
+    _check(load_library().hy_encode_weights(p, ctypes.byref(s), Wc.ctypes.data, ctypes.byref(out)),
+           "hy_encode_weights")
+    return out.value
+
+
+def hy_weights_layout(w: int) -> hy_layout:
+    lay = hy_layout()
+    _check(load_library().hy_weights_layout(w, ctypes.byref(lay)), "hy_weights_layout")
+    return lay
+
+
+def hy_weights_destroy(w: int):
+    load_library().hy_weights_destroy(w)
+
+
+def hy_conv_eval(w: int, ct_in, ct_out, J: Optional[int] = None, Jout: Optional[int] = None, stream=None):
+    J = ct_in.shape[0] if J is None else J
+    Jout = ct_out.shape[0] if Jout is None else Jout
+    _check(load_library().hy_conv_eval(w, _dev_ptr(ct_in), J, _dev_ptr(ct_out), Jout, _stream(stream)),
+           "hy_conv_eval")
+
+
+def hy_conv_eval_host(w: int, ct_in: np.ndarray, ct_out: np.ndarray, stream=None):
+    assert ct_in.dtype == np.uint64 and ct_out.dtype == np.uint64
+    assert ct_in.flags.c_contiguous and ct_out.flags.c_contiguous
+    _check(load_library().hy_conv_eval_host(w, ct_in.ctypes.data, ct_in.shape[0], ct_out.ctypes.data,
+                                            ct_out.shape[0], _stream(stream)), "hy_conv_eval_host")
+
+
+def hy_poly_mul(p: int, a, b, c, stream=None):
+    _check(load_library().hy_poly_mul(p, _dev_ptr(a), _dev_ptr(b), _dev_ptr(c), a.shape[0], _stream(stream)),
+           "hy_poly_mul")
+
+
+def hy_ntt_roundtrip(p: int, x, stream=None):
+    _check(load_library().hy_ntt_roundtrip(p, _dev_ptr(x), x.shape[0], _stream(stream)), "hy_ntt_roundtrip")
+
+
+def hy_rotate(p: int, ct_in, galois_elt: int, ct_out, stream=None):
+    _check(load_library().hy_rotate(p, _dev_ptr(ct_in), galois_elt, _dev_ptr(ct_out), ct_in.shape[0],
+                                    _stream(stream)), "hy_rotate")
+
+
+def hy_decrypt_debug(p: int, sk: np.ndarray, ct, scale: int) -> np.ndarray:
+    """Returns uint64 [n][N] slot values (row 0 then row 1) times scale^{-1} mod t."""
+    s = np.ascontiguousarray(sk, dtype=np.int8)
+    n, N = ct.shape[0], ct.shape[-1]
+    out = np.empty((n, N), dtype=np.uint64)
+    _check(load_library().hy_decrypt_debug(p, s.ctypes.data, _dev_ptr(ct), n, scale, out.ctypes.data),
+           "hy_decrypt_debug")
+    return out
+
+
+def hy_kernel_launches() -> int:
+    return int(load_library().hy_kernel_launches())
+
+
+def hy_weights_set_stage_events(w: int, events: Sequence) -> None:
+    """events: torch.cuda.Event objects (created with enable_timing=True), at most 5."""
+    arr = (ctypes.c_void_p * max(1, len(events)))(*[int(e.cuda_event) for e in events])
+    _check(load_library().hy_weights_set_stage_events(w, arr, len(events)), "hy_weights_set_stage_events")

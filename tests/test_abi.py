@@ -1,0 +1,96 @@
+"""C-ABI checks that need no GPU: the library builds/loads, exports every symbol include/hyena.h
+declares, and its host-only layout planner agrees with the oracle's (independent implementations)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import conv
+from oracle.params import find_k, h_pn
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def hy():
+    from paper_2311_12519_b200 import build
+    build.build()
+    import paper_2311_12519_b200 as pkg
+    pkg.load_library()
+    return pkg
+
+
+def declared_symbols():
+    txt = open(os.path.join(ROOT, "include", "hyena.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:hy_status|void|uint64_t|const char\*)\s+(hy_\w+)\s*\(", txt, re.M)))
+
+
+def test_exports_every_declared_symbol(hy):
+    names = declared_symbols()
+    assert len(names) >= 14
+    lib = ctypes.CDLL(hy.library_path())
+    for n in names:
+        assert hasattr(lib, n), n
+    assert sorted(hy.EXPORTED) == names
+    out = subprocess.run(["nm", "-D", "--defined-only", hy.library_path()], capture_output=True, text=True).stdout
+    for n in names:
+        assert re.search(rf"\bT {n}\b", out), n
+
+
+def test_sm100a_code_in_library(hy):
+    out = subprocess.run(["cuobjdump", "--list-elf", hy.library_path()], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+CFGS = synth.configs()
+
+
+@pytest.mark.parametrize("name", sorted(CFGS))
+def test_planner_matches_oracle(hy, name):
+    c = CFGS[name]
+    lay = hy.hy_plan_layout(c.N, c.t, **c.shape_dict())
+    p = conv.plan(c.N, c.batch, c.Ci, c.Co, c.H, c.W, c.kh, c.kw, c.pad, c.depthwise, c.force_cn)
+    got = (lay.Wp, lay.Hp, lay.mode, lay.per_row, lay.Hb, lay.Hv, lay.bands, lay.G, lay.cn, lay.U, lay.Jc, lay.Jo,
+           lay.J, lay.Jout, lay.Hout, lay.Wout)
+    exp = (p.Wp, p.Hp, 0 if p.mode == "blocks" else 1, p.per_row, p.Hb, p.Hv, p.bands, p.G, p.cn, p.U, p.Jc, p.Jo,
+           p.J, p.Jout, p.Hout, p.Wout)
+    assert got == exp
+    assert list(lay.tap_step[:lay.n_taps]) == [s for _, _, s in p.taps]
+    ls = conv.setup(p, c.t)
+    assert list(lay.galois[:lay.n_galois]) == ls.galois
+    assert (lay.k, lay.scale, lay.sign_coeff) == (ls.k, ls.scale, ls.sign_coeff)
+
+
+def test_library_h_and_k_match_oracle(hy):
+    """The library's closed-form h (-(w + w^3)/2) equals the oracle's by-encoding h."""
+    for N in (1024, 4096, 16384):
+        lay = hy.hy_plan_layout(N, 65537, Ci=2, Co=2, H=4, W=4, kh=3, kw=3, pad=1, batch=1)
+        assert lay.h == h_pn(65537, N)
+        assert lay.k == find_k(65537, lay.h)
+
+
+def test_planner_rejects_bad_shapes(hy):
+    with pytest.raises(hy.HyenaError, match="stride"):
+        hy.hy_plan_layout(4096, 65537, Ci=2, Co=2, H=4, W=4, kh=3, kw=3, pad=1, batch=1, stride=2)
+    with pytest.raises(hy.HyenaError, match="empty"):
+        hy.hy_plan_layout(4096, 65537, Ci=0, Co=2, H=4, W=4, kh=3, kw=3, pad=1, batch=1)
+    with pytest.raises(hy.HyenaError, match="prime"):
+        hy.hy_plan_layout(4096, 65539, Ci=2, Co=2, H=4, W=4, kh=3, kw=3, pad=1, batch=1)
+    with pytest.raises(hy.HyenaError, match="k must"):
+        hy.hy_plan_layout(4096, 65537, Ci=2, Co=2, H=4, W=4, kh=3, kw=3, pad=1, batch=1, k=33)
+    with pytest.raises(hy.HyenaError, match="exceeds a slot row"):
+        hy.hy_plan_layout(1024, 65537, Ci=2, Co=2, H=4, W=1000, kh=3, kw=3, pad=1, batch=1)
+
+
+def test_params_create_validation_without_gpu(hy):
+    """Argument validation happens before any device call."""
+    with pytest.raises(hy.HyenaError, match="not prime"):
+        hy.hy_params_create(4096, [2**59 + 1], 65537)
+    with pytest.raises(hy.HyenaError, match="1 mod 2N"):
+        hy.hy_params_create(4096, [2147483647], 65537)            # 2^31-1: prime, not 1 mod 8192
+    with pytest.raises(hy.HyenaError, match=r"\(2\^20, 2\^60\)"):
+        hy.hy_params_create(4096, [2305843009213693951], 65537)   # 2^61-1: prime but too large

@@ -1,0 +1,136 @@
+"""GPU parity of the whole encrypted convolution (hy_conv_eval) vs the oracle (T2):
+ciphertext limbs bit-exact, and decryption = plain convolution mod t.  Marked gpu."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import bfv, conv
+from oracle.params import ntt_primes
+from tests.hyena_client import check_decrypted, layer_from_config, make_layer
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def hy():
+    import paper_2311_12519_b200 as pkg
+    from paper_2311_12519_b200 import build
+    build.build()
+    pkg.load_library()
+    assert torch.cuda.is_available()
+    return pkg
+
+
+def run_gpu(hy, lay, shape_kw, units=None):
+    p = hy.hy_params_create(lay.P.N, lay.P.primes, lay.P.t, 0)
+    try:
+        elts = list(lay.keys)
+        if elts:
+            hy.hy_keys_upload(p, elts, np.stack([lay.keys[g] for g in elts]))
+        w = hy.hy_encode_weights(p, lay.W, **shape_kw)
+        try:
+            L = hy.hy_weights_layout(w)
+            assert (L.J, L.Jout, L.cn, L.k) == (lay.plan.J, lay.plan.Jout, lay.plan.cn, lay.ls.k)
+            nu = L.U if units is None else units
+            ct_in = torch.from_numpy(lay.ct_in[: nu * L.Jc]).cuda()
+            ct_out = torch.full((nu * L.Jo, 2, lay.P.L, lay.P.N), 7, dtype=torch.uint64, device="cuda")
+            hy.hy_conv_eval(w, ct_in, ct_out)
+            torch.cuda.synchronize()
+            got = ct_out.cpu().numpy()
+            # library debug decryption of everything (checked against the plain conv below)
+            dec = hy.hy_decrypt_debug(p, lay.s.astype(np.int8), ct_out, L.scale)
+            # end-to-end host API gives the same bytes
+            host_out = np.zeros_like(got)
+            hy.hy_conv_eval_host(w, np.ascontiguousarray(lay.ct_in[: nu * L.Jc]), host_out)
+            assert np.array_equal(host_out, got)
+            return got, dec, L
+        finally:
+            hy.hy_weights_destroy(w)
+    finally:
+        hy.hy_params_destroy(p)
+
+
+def shape_of(lay):
+    p = lay.plan
+    return dict(Ci=p.Ci, Co=p.Co, H=p.H, W=p.W, kh=p.kh, kw=p.kw, pad=p.pad, depthwise=int(p.depthwise),
+                batch=p.batch, k=lay.ls.k if p.cn == 2 else 0, force_cn=p.cn)
+
+
+def check_plain_from_library_decrypt(lay, dec):
+    p = lay.plan
+    got = conv.unpack(p, dec.astype(np.int64))
+    from tests.hyena_client import expected_plain
+    exp = expected_plain(lay)
+    sel = (slice(None),) * 4
+    assert np.array_equal(got, exp)
+
+
+CASES = {
+    "cn2_blocks": dict(N=1024, bits=50, L=2, batch=2, Ci=4, Co=4, H=5, W=5, kh=3, kw=3, pad=1),
+    "cn2_k1": dict(N=1024, bits=50, L=2, batch=1, Ci=4, Co=6, H=6, W=6, kh=3, kw=3, pad=1, k=1),
+    "cn2_odd_channels": dict(N=2048, bits=60, L=3, batch=1, Ci=3, Co=5, H=7, W=7, kh=3, kw=3, pad=1),
+    "cn1_bands": dict(N=1024, bits=50, L=2, batch=1, Ci=3, Co=2, H=20, W=20, kh=3, kw=3, pad=1),
+    "cn1_blocks_tail": dict(N=1024, bits=50, L=2, batch=5, Ci=2, Co=3, H=6, W=6, kh=3, kw=3, pad=1, force_cn=1),
+    "dw_cn2": dict(N=1024, bits=50, L=2, batch=2, Ci=4, Co=4, H=6, W=6, kh=3, kw=3, pad=1, depthwise=True),
+    "dw_cn1": dict(N=1024, bits=50, L=2, batch=9, Ci=3, Co=3, H=6, W=6, kh=3, kw=3, pad=1, depthwise=True),
+    "pw_cn1": dict(N=1024, bits=50, L=2, batch=9, Ci=5, Co=4, H=6, W=6, kh=1, kw=1, pad=0),
+    "pw_cn2": dict(N=1024, bits=50, L=2, batch=2, Ci=4, Co=4, H=6, W=6, kh=1, kw=1, pad=0),
+    "k5x5": dict(N=2048, bits=50, L=2, batch=1, Ci=2, Co=2, H=8, W=8, kh=5, kw=5, pad=2),
+    "wide_weights": dict(N=2048, bits=60, L=3, batch=1, Ci=8, Co=8, H=6, W=6, kh=3, kw=3, pad=1,
+                         xrange=(-128, 128), wrange=(-128, 128)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_conv_bit_exact_small(hy, name):
+    c = dict(CASES[name])
+    N, bits, L = c.pop("N"), c.pop("bits"), c.pop("L")
+    lay = make_layer(N, ntt_primes(N, bits, L), seed=500 + sorted(CASES).index(name), **c)
+    got, dec, Lay = run_gpu(hy, lay, shape_of(lay))
+    ref = conv.he_conv(lay.P, lay.ls, lay.W, lay.ct_in, lay.keys)
+    for i in range(Lay.Jout):
+        assert np.array_equal(got[i], ref[i]), f"output ct {i} differs"
+    check_decrypted(lay, {i: got[i] for i in range(Lay.Jout)})
+    check_plain_from_library_decrypt(lay, dec)
+
+
+def test_conv_partial_units(hy):
+    """hy_conv_eval on a prefix of the units (the sharding primitive) = the same outputs."""
+    c = dict(CASES["cn1_blocks_tail"])
+    N, bits, L = c.pop("N"), c.pop("bits"), c.pop("L")
+    lay = make_layer(N, ntt_primes(N, bits, L), seed=550, **c)
+    got, _, Lay = run_gpu(hy, lay, shape_of(lay), units=1)
+    ref = conv.he_conv(lay.P, lay.ls, lay.W, lay.ct_in, lay.keys, out_cts=list(range(Lay.Jo)))
+    for i in range(Lay.Jo):
+        assert np.array_equal(got[i], ref[i])
+
+
+def test_c1_config_full(hy):
+    """BASELINE configs[0] (C1) end to end: full ciphertext parity + decryption."""
+    lay = layer_from_config(synth.configs()["C1"])
+    got, dec, Lay = run_gpu(hy, lay, synth.configs()["C1"].shape_dict())
+    ref = conv.he_conv(lay.P, lay.ls, lay.W, lay.ct_in, lay.keys)
+    for i in range(Lay.Jout):
+        assert np.array_equal(got[i], ref[i])
+    check_plain_from_library_decrypt(lay, dec)
+
+
+def test_shape_errors(hy):
+    c = dict(CASES["cn2_blocks"])
+    N, bits, L = c.pop("N"), c.pop("bits"), c.pop("L")
+    lay = make_layer(N, ntt_primes(N, bits, L), seed=560, **c)
+    p = hy.hy_params_create(N, lay.P.primes, 65537)
+    try:
+        w = hy.hy_encode_weights(p, lay.W, **shape_of(lay))
+        try:
+            x = torch.zeros((3, 2, L, N), dtype=torch.uint64, device="cuda")
+            with pytest.raises(hy.HyenaError, match="multiple of Jc"):
+                hy.hy_conv_eval(w, x, x)
+            x2 = torch.zeros((2, 2, L, N), dtype=torch.uint64, device="cuda")
+            with pytest.raises(hy.HyenaError, match="no Galois key"):
+                hy.hy_conv_eval(w, x2, x2)
+        finally:
+            hy.hy_weights_destroy(w)
+    finally:
+        hy.hy_params_destroy(p)

@@ -101,7 +101,7 @@ void hy_params_destroy(hy_params* p);
 /* Upload server-side switching keys generated by the client (PAPER.md:883-884, 1474-1475 [app]).
  * keys: [n_elts][L digits][2: b, a][L limbs][N] uint64, COEFFICIENT form, canonical residues;
  * key for element g satisfies b_{i,l} + a_{i,l} s = e_i + [i == l] s(X^g)  (mod q_l)
- * (RNS-digit gadget, reading R3).  keys_on_device != 0: `keys` is a device pointer.
+ * (RNS-digit gadget, reading R5).  keys_on_device != 0: `keys` is a device pointer.
  * The library converts them to NTT form with Shoup companions and keeps its own copy;
  * re-uploading an element replaces it.  Synchronises the device.  Errors: HY_EINVAL
  * (even or out-of-range element, too many elements), HY_ENOMEM, HY_ECUDA. */

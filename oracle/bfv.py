@@ -8,8 +8,8 @@ Follows PAPER.md §2.3 (lines 236-378):
   * HRot = automorphism + key switching with a decomposition, hoisted
     (decompose once, then per-rotation automorphism + key inner product; PAPER.md:373-378,
     :1472-1473 "PermDecomp"/"PermAuto").
-Readings: RNS digits, one per limb, no special prime (R3); hoisted digit
-definition d_i = [c1]_{q_i} taken BEFORE the automorphism (R4); ternary secret and
+Readings: RNS digits, one per limb, no special prime (R5); hoisted digit
+definition d_i = [c1]_{q_i} taken BEFORE the automorphism (R6); ternary secret and
 CBD errors come from synth/ and are passed in (R2).
 
 Ciphertexts are uint64 arrays [2][L][N] of canonical residues (coefficient form).
@@ -112,7 +112,7 @@ def noise_budget_bits(P: BFVParams) -> float:
 
 
 def galois_keygen(P: BFVParams, s, g: int, a, e) -> np.ndarray:
-    """Switching key for X -> X^g under the RNS-digit gadget (reading R3):
+    """Switching key for X -> X^g under the RNS-digit gadget (reading R5):
     digit i, limb l:  b_{i,l} = [-a_{i,l} s + e_i + [i == l] s(X^g)]_{q_l},  a_{i,l} uniform.
     [i == l] is the residue mod q_l of the gadget g_i = (Q/q_i)[(Q/q_i)^{-1}]_{q_i}.
     a: uint64 [L][L][N], e: [L][N].  Returns uint64 [L][2][L][N] (b first, then a)."""
@@ -139,7 +139,7 @@ def decompose(P: BFVParams, ct) -> List[np.ndarray]:
 def rotate_hoisted(P: BFVParams, ct, digits, g: int, key) -> np.ndarray:
     """Hoisting step 2 ('PermAuto'): for every limb l
         c0' = [sigma_g(c0) + sum_i sigma_g(d_i) b_{i,l}]_{q_l},   c1' = [sum_i sigma_g(d_i) a_{i,l}]_{q_l}
-    with sigma_g applied to the integer digit polynomials (reading R4)."""
+    with sigma_g applied to the integer digit polynomials (reading R6)."""
     L, N = P.L, P.N
     dg = [ring.automorphism(d, g) for d in digits]
     out = np.empty((2, L, N), dtype=np.uint64)

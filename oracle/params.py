@@ -107,7 +107,7 @@ def centered(x: int, p: int) -> int:
 
 def find_k(p: int, h: int, k_max: int = 32) -> int:
     """k in [1, k_max] minimising |[k h]_p| (centered), ties -> smaller k.
-    k_max = 32 is DESIGN.md reading R6 (the paper's k=11 needs 11 <= k_max <= 50)."""
+    k_max = 32 is DESIGN.md reading R13 (the paper's k=11 needs 11 <= k_max <= 50)."""
     best, best_k = None, None
     for k in range(1, k_max + 1):
         v = abs(centered(k * h, p))

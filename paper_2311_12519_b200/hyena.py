@@ -225,5 +225,8 @@ def hy_kernel_launches() -> int:
 
 def hy_weights_set_stage_events(w: int, events: Sequence) -> None:
     """events: torch.cuda.Event objects (created with enable_timing=True), at most 5."""
+    for e in events:            # torch creates the cudaEvent_t lazily, on its first record()
+        if int(e.cuda_event) == 0:
+            e.record()
     arr = (ctypes.c_void_p * max(1, len(events)))(*[int(e.cuda_event) for e in events])
     _check(load_library().hy_weights_set_stage_events(w, arr, len(events)), "hy_weights_set_stage_events")

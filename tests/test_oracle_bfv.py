@@ -1,5 +1,5 @@
 """Pins for oracle/bfv.py: decryption correctness, homomorphic properties, hoisted rotation,
-and the hoisted-vs-direct distinction (reading R4) — CPU only, small N."""
+and the hoisted-vs-direct distinction (reading R6) — CPU only, small N."""
 import numpy as np
 import pytest
 

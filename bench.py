@@ -144,7 +144,7 @@ def run_gpu(args, cfg, rank, world):
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=f"cuda:{dev}")  # > 126 MB L2
 
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     hy.hy_weights_set_stage_events(w, ev)
     for _ in range(args.warmup):
         hy.hy_conv_eval(w, ct_in, ct_out)
@@ -154,15 +154,15 @@ def run_gpu(args, cfg, rank, world):
         import torch.distributed as dist
         dist.barrier()
     torch.cuda.synchronize()
-    step_ms, stage_ms = [], [[] for _ in range(4)]
+    step_ms, stage_ms = [], [[] for _ in range(3)]
     launches0 = hy.hy_kernel_launches()
     with ClockSampler(dev) as clk:
         for _ in range(args.steps):
             flush.zero_()                       # L2 flushed between timed iterations (untimed)
             hy.hy_conv_eval(w, ct_in, ct_out)
-            ev[4].synchronize()
-            step_ms.append(ev[0].elapsed_time(ev[4]))
-            for i in range(4):
+            ev[3].synchronize()
+            step_ms.append(ev[0].elapsed_time(ev[3]))
+            for i in range(3):
                 stage_ms[i].append(ev[i].elapsed_time(ev[i + 1]))
     torch.cuda.synchronize()
     launches = hy.hy_kernel_launches() - launches0
@@ -202,13 +202,13 @@ def run_gpu(args, cfg, rank, world):
 def roofline(cfg, res, peaks):
     """Roofline of the dominant stage (largest mean time)."""
     w = res["work"]
-    names = ["S1_permdecomp", "S2_permauto", "S3_mac_wht", "S4S5_align_intt"]
+    names = ["S1_permdecomp", "S2S3_ksmac_wht", "S4S5_align_intt"]
     st = res["stage_ms"]
     dom = int(np.argmax(st))
     clk = res["clocks"]
     clk_mhz = peaks.get("sm_max_mhz", 1965.0)
-    if dom == 2:
-        achieved = w["dfma"] / (st[2] * 1e-3) / 1e12
+    if dom == 1:
+        achieved = w["dfma"] / (st[1] * 1e-3) / 1e12
         peak = DFMA_PER_CLK_SM * SM_COUNT * clk_mhz * 1e6 / 1e12
         return {"kernel": names[dom], "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TDFMA/s",
                 "frac": achieved / peak, "traffic": None,
@@ -216,11 +216,7 @@ def roofline(cfg, res, peaks):
                              "(derived; DESIGN.md)"}
     L, N = len(cfg.primes), cfg.N
     lay = res["lay"]
-    if dom == 1:
-        T = lay.n_taps
-        # per rotated coefficient: read L digits + C0 (gathered), 2L key words + 2L Shoup words, write 2
-        bytes_ = lay.J * T * L * N * 8 * ((L + 1) + 4 * L + 2)
-    elif dom == 0:
+    if dom == 0:
         bytes_ = lay.J * (2 * L * N * 8 + (L * L + L) * N * 8)
     else:
         bytes_ = lay.Jout * (3 * 2 * L * N * 8)
@@ -339,7 +335,7 @@ def main():
                        "Jout": lay.Jout, "rotations": work["rotations"], "rowswaps": work["rowswaps"],
                        "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"replicas x{world}"},
             "ct_mac_gops": gops,
-            "stages_ms": dict(zip(["S1_permdecomp", "S2_permauto", "S3_mac_wht", "S4S5_align_intt"],
+            "stages_ms": dict(zip(["S1_permdecomp", "S2S3_ksmac_wht", "S4S5_align_intt"],
                                   res["stage_ms"])),
             "roofline": roofline(cfg, res, peaks),
             "gpu_launches": res["launches"],

@@ -138,7 +138,7 @@ hy_status hy_conv_eval_host(hy_weights* w, const uint64_t* ct_in_host, size_t J,
 /* Per-stage entry points (for per-kernel parity tests; same kernels as hy_conv_eval).
  * hy_poly_mul: c = a * b in Z_{q_l}[X]/(X^N+1) for n polynomial pairs, all device
  *   [n][L][N] coefficient form (forward NTT, pointwise Shoup product, inverse NTT).
- * hy_ntt_roundtrip: x -> INTT(NTT(x)) in place, device [n][L][N].
+ * hy_ntt_roundtrip: x -> INTT(NTT(x)) in place, device [n][L][N] (synchronises the stream).
  * hy_rotate: hoisted HRot of n ciphertexts by Galois element g (key must be uploaded):
  *   device [n][2][L][N] -> device [n][2][L][N], coefficient form. */
 hy_status hy_poly_mul(const hy_params* p, const uint64_t* a, const uint64_t* b, uint64_t* c, size_t n,
@@ -148,9 +148,9 @@ hy_status hy_rotate(hy_params* p, const uint64_t* ct_in, uint32_t galois_elt, ui
                     void* cuda_stream);
 
 /* Measurement hooks (bench.py): total number of kernels this library has launched in the
- * process, and optional CUDA events (cudaEvent_t cast to void*) that hy_conv_eval records on
- * its stream at the stage boundaries [before S1, after S1, after S2, after S3, after S4+S5].
- * n = 0 clears them.  Errors: HY_EINVAL. */
+ * process, and optional CUDA events (cudaEvent_t cast to void*, at most 4) that hy_conv_eval
+ * records on its stream at the stage boundaries [before S1, after S1, after the fused S2+S3,
+ * after S4+S5].  n = 0 clears them.  Errors: HY_EINVAL. */
 uint64_t hy_kernel_launches(void);
 hy_status hy_weights_set_stage_events(hy_weights* w, void* const* events, uint32_t n);
 

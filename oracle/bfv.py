@@ -62,6 +62,14 @@ def crt(residues: Sequence[np.ndarray], primes: Sequence[int]) -> list:
     return [x % Q for x in out]
 
 
+def _mul_sparse_first(x, y, q: int) -> np.ndarray:
+    """x * y mod (X^N + 1, q), passing the operand with fewer nonzero coefficients first (the
+    schoolbook product skips zero coefficients of its first operand; the product commutes)."""
+    if np.count_nonzero(np.asarray(y)) < np.count_nonzero(np.asarray(x)):
+        x, y = y, x
+    return ring.nc_mul(x, y, q)
+
+
 def encrypt(P: BFVParams, m, s, a, e) -> np.ndarray:
     """Symmetric BFV encryption: c0 = [Delta m + a s + e], c1 = [-a], per limb.
     m: [N] ints in [0,t); s: [N] ternary; a: uint64 [L][N] uniform residues; e: [N] small ints."""
@@ -69,7 +77,7 @@ def encrypt(P: BFVParams, m, s, a, e) -> np.ndarray:
     ct = np.empty((2, L, N), dtype=np.uint64)
     m = [int(x) % P.t for x in m]
     for l, q in enumerate(P.primes):
-        a_s = ring.nc_mul(s, a[l], q)  # ternary s first: its zero terms are skipped
+        a_s = _mul_sparse_first(s, a[l], q)
         dm = np.array([(P.delta * x) % q for x in m], dtype=object)
         ct[0, l] = ((dm + a_s.astype(object) + np.asarray(e, dtype=np.int64).astype(object)) % q).astype(np.uint64)
         ct[1, l] = ring.canon(-(a[l].astype(object)), q)
@@ -121,7 +129,7 @@ def galois_keygen(P: BFVParams, s, g: int, a, e) -> np.ndarray:
     key = np.empty((L, 2, L, N), dtype=np.uint64)
     for i in range(L):
         for l, q in enumerate(P.primes):
-            a_s = ring.nc_mul(s, a[i, l], q)
+            a_s = _mul_sparse_first(s, a[i, l], q)
             b = -(a_s.astype(object)) + np.asarray(e[i], dtype=np.int64).astype(object)
             if i == l:
                 b = b + s_g.astype(object)

@@ -99,6 +99,22 @@ u64 root_2n(u64 q, uint32_t N) {
 
 using namespace hyhost;
 
+// g = 3^s (swap 0) or -3^s (swap 1) mod 2N with s in [0, N/2): Z_{2N}^* = <3> x <-1>
+bool hy_galois_act(uint32_t g, uint32_t N, GaloisAct* out) {
+  const u64 two_n = 2 * (u64)N;
+  if (!(g & 1) || g >= two_n) return false;
+  u64 e = 1;
+  for (uint32_t s = 0; s < N / 2; s++) {
+    if (e == g || two_n - e == g) {
+      out->shift = s;
+      out->swap = (e == g) ? 0u : 1u;
+      return true;
+    }
+    e = e * 3 % two_n;
+  }
+  return false;
+}
+
 static uint32_t next_pow2(uint32_t x) {
   uint32_t r = 1;
   while (r < x) r <<= 1;
@@ -281,12 +297,33 @@ extern "C" hy_status hy_params_create(uint32_t N, const uint64_t* q, uint32_t L,
     c.c30_sh = shoup(c.c30, ql);
     c.off = ql * (((1ull << 59) + ql - 1) / ql);
   }
+  // slot-order position j <-> bit-reversed butterfly position k, split into the
+  // NTT blocks of HY_NTT_BLOCK coefficients
+  std::vector<int32_t> kos(N), own_j, own_k;
+  {
+    u64 e = 1;
+    for (uint32_t j = 0; j < N / 2; j++) {
+      kos[j] = (int32_t)bitrev((uint32_t)((e - 1) / 2), p->logN);
+      const u64 en = 2 * (u64)N - e;
+      kos[j + N / 2] = (int32_t)bitrev((uint32_t)((en - 1) / 2), p->logN);
+      e = e * 3 % (2 * (u64)N);
+    }
+    const uint32_t B = N < HY_NTT_BLOCK ? N : HY_NTT_BLOCK, S = N / B;
+    for (uint32_t h = 0; h < S; h++)
+      for (uint32_t j = 0; j < N; j++)
+        if ((uint32_t)kos[j] / B == h) {
+          own_j.push_back((int32_t)j);
+          own_k.push_back((int32_t)(kos[j] - h * B));
+        }
+  }
   const size_t bytes = (size_t)L * N * sizeof(u64);
   hy_status st;
   if ((st = upload((void**)&p->tab.psi_rev, psi_rev.data(), bytes)) != HY_OK ||
       (st = upload((void**)&p->tab.psi_rev_sh, psi_rev_sh.data(), bytes)) != HY_OK ||
       (st = upload((void**)&p->tab.ipsi_rev, ipsi_rev.data(), bytes)) != HY_OK ||
-      (st = upload((void**)&p->tab.ipsi_rev_sh, ipsi_rev_sh.data(), bytes)) != HY_OK) {
+      (st = upload((void**)&p->tab.ipsi_rev_sh, ipsi_rev_sh.data(), bytes)) != HY_OK ||
+      (st = upload((void**)&p->tab.own_j, own_j.data(), N * sizeof(int32_t))) != HY_OK ||
+      (st = upload((void**)&p->tab.own_k, own_k.data(), N * sizeof(int32_t))) != HY_OK) {
     hy_params_destroy(p);
     return st;
   }
@@ -307,6 +344,8 @@ extern "C" void hy_params_destroy(hy_params* p) {
   cudaFree(p->tab.psi_rev_sh);
   cudaFree(p->tab.ipsi_rev);
   cudaFree(p->tab.ipsi_rev_sh);
+  cudaFree(p->tab.own_j);
+  cudaFree(p->tab.own_k);
   for (auto& kv : p->keys) cudaFree(kv.second.ntt);
   delete p;
 }
@@ -388,10 +427,10 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
     w->K = (int)lay.Jc * T;
     w->wblocks = 1;
   }
-  const int tm = w->M >= 16 ? 16 : (w->M >= 8 ? 8 : (w->M >= 4 ? 4 : (w->M >= 2 ? 2 : 1)));
-  const int Mpad = (w->M + tm - 1) / tm * tm;
-  // weight tables (S0): row layout documented in DESIGN.md
-  std::vector<int32_t> wm((size_t)w->wblocks * Mpad * w->K, 0);
+  w->Mpad = hy_mac_mpad(w->M);
+  w->Kpad = (w->K + 15) / 16 * 16;  // multiple of every K chunk (2 WM <= 16)
+  // weight table (S0), [block][kk][row] as exact doubles; row semantics documented in DESIGN.md §4
+  std::vector<double> wt((size_t)w->wblocks * w->Kpad * w->Mpad, 0.0);
   const uint32_t Ci = sh->Ci, Co = dw ? sh->Ci : sh->Co, kw = sh->kw;
   auto Wat = [&](uint32_t o, uint32_t c, int tau) -> int32_t {
     const uint32_t dy = tau / kw, dx = tau % kw;
@@ -408,14 +447,14 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
         } else if (lay.cn == 2) {
           // row = (g*2 + d)*2 + c : slot row c of diagonal d pairs input 2j+c with output 2g+(c^d)
           const int g = row / 4, d = (row / 2) % 2, c = row % 2;
-          const int j = kk / T, tau = kk % T;
+          const int tau = kk / (int)lay.Jc, j = kk % (int)lay.Jc;  // K axis tap-major
           v = Wat(2 * g + (c ^ d), 2 * j + c, tau);
         } else {
-          v = Wat(row, kk / T, kk % T);
+          v = Wat(row, kk % (int)lay.Jc, kk / (int)lay.Jc);
         }
-        wm[((size_t)b * Mpad + row) * w->K + kk] = v;
+        wt[((size_t)b * w->Kpad + kk) * w->Mpad + row] = (double)v;
       }
-  hy_status st = upload((void**)&w->d_wm, wm.data(), wm.size() * sizeof(int32_t));
+  hy_status st = upload((void**)&w->d_wt, wt.data(), wt.size() * sizeof(double));
   if (st != HY_OK) {
     hy_weights_destroy(w);
     return st;
@@ -453,7 +492,6 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
   } allocs[] = {
       {&w->d_D, Jin * L * L * N},
       {&w->d_C0, Jin * L * N},
-      {&w->d_R, Jin * T * ctw},
       {&w->d_P, Jo * ctw * ((lay.cn == 2 && !dw) ? 2 : 1)},
       {&w->d_D2, (lay.cn == 2 && !dw) ? Jo * L * L * N + Jo * L * N : 0},
       {&w->d_in, Jin * ctw},
@@ -469,7 +507,7 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
     }
   }
   HY_CUDA_TRY(cudaMalloc(&w->d_tap_keys, T * sizeof(u64*)));
-  HY_CUDA_TRY(cudaMalloc(&w->d_tap_g, T * sizeof(uint32_t)));
+  HY_CUDA_TRY(cudaMalloc(&w->d_tap_act, T * sizeof(GaloisAct)));
   w->keys_version = ~0ull;
   HY_CUDA_TRY(cudaDeviceSynchronize());
   *out = w;
@@ -477,7 +515,7 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
 }
 
 extern "C" hy_status hy_weights_set_stage_events(hy_weights* w, void* const* events, uint32_t n) {
-  HY_CHECK(w && (n == 0 || events) && n <= 5, HY_EINVAL, "bad stage events");
+  HY_CHECK(w && (n == 0 || events) && n <= 4, HY_EINVAL, "bad stage events");
   for (uint32_t i = 0; i < n; i++) w->ev[i] = (cudaEvent_t)events[i];
   w->n_ev = n;
   return HY_OK;
@@ -492,17 +530,16 @@ extern "C" hy_status hy_weights_layout(const hy_weights* w, hy_layout* out) {
 extern "C" void hy_weights_destroy(hy_weights* w) {
   if (!w) return;
   cudaSetDevice(w->p->device);
-  cudaFree(w->d_wm);
+  cudaFree(w->d_wt);
   cudaFree(w->d_sign);
   cudaFree(w->d_D);
   cudaFree(w->d_C0);
-  cudaFree(w->d_R);
   cudaFree(w->d_P);
   cudaFree(w->d_D2);
   cudaFree(w->d_in);
   cudaFree(w->d_out);
   cudaFree(w->d_tap_keys);
-  cudaFree(w->d_tap_g);
+  cudaFree(w->d_tap_act);
   delete w;
 }
 
@@ -512,7 +549,7 @@ static hy_status bind_keys(hy_weights* w) {
   const hy_layout& lay = w->lay;
   const uint32_t row = p->N / 2;
   std::vector<u64*> ptrs(lay.n_taps, nullptr);
-  std::vector<uint32_t> gs(lay.n_taps, 1);
+  std::vector<GaloisAct> acts(lay.n_taps, GaloisAct{0u, 0u});
   for (uint32_t tau = 0; tau < lay.n_taps; tau++) {
     const int64_t st = (((int64_t)lay.tap_step[tau] % (int64_t)row) + row) % row;
     if (st == 0) continue;
@@ -521,7 +558,7 @@ static hy_status bind_keys(hy_weights* w) {
     HY_CHECK(it != p->keys.end(), HY_ENOKEY, "no Galois key for element %u (tap %u, step %d)", g, tau,
              lay.tap_step[tau]);
     ptrs[tau] = it->second.ntt;
-    gs[tau] = g;
+    HY_CHECK(hy_galois_act(g, p->N, &acts[tau]), HY_EINVAL, "bad Galois element %u", g);
   }
   w->d_swap_key = nullptr;
   if (lay.cn == 2 && !w->shape.depthwise) {
@@ -530,7 +567,7 @@ static hy_status bind_keys(hy_weights* w) {
     w->d_swap_key = it->second.ntt;
   }
   HY_CUDA_TRY(cudaMemcpy(w->d_tap_keys, ptrs.data(), ptrs.size() * sizeof(u64*), cudaMemcpyHostToDevice));
-  HY_CUDA_TRY(cudaMemcpy(w->d_tap_g, gs.data(), gs.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  HY_CUDA_TRY(cudaMemcpy(w->d_tap_act, acts.data(), acts.size() * sizeof(GaloisAct), cudaMemcpyHostToDevice));
   w->keys_version = p->keys_version;
   return HY_OK;
 }
@@ -557,12 +594,10 @@ extern "C" hy_status hy_conv_eval(hy_weights* w, const uint64_t* ct_in, size_t J
   HY_TRY(mark(0));
   HY_TRY(hyk::permdecomp(p, ct_in, J, w->d_D, w->d_C0, s));  // S1 PermDecomp
   HY_TRY(mark(1));
-  HY_TRY(hyk::permauto(p, w->d_D, w->d_C0, J, (int)lay.n_taps, w->d_tap_keys, w->d_tap_g, w->d_R, s));  // S2
+  HY_TRY(hyk::ksmac(w, nu, s));  // S2 PermAuto fused with S3 lazy MAC + WHT + reduce + sign PMult
   HY_TRY(mark(2));
-  HY_TRY(hyk::mac(w, nu, s));  // S3 lazy MAC + WHT + reduce + sign PMult
-  HY_TRY(mark(3));
   HY_TRY(hyk::finish_outputs(w, nu, ct_out, s));  // S4 alignment + S5 INTT
-  HY_TRY(mark(4));
+  HY_TRY(mark(3));
   return HY_OK;
 }
 
@@ -607,8 +642,16 @@ extern "C" hy_status hy_ntt_roundtrip(const hy_params* p, uint64_t* x, size_t n,
   if (n == 0) return HY_OK;
   HY_CUDA_TRY(cudaSetDevice(p->device));
   cudaStream_t s = (cudaStream_t)stream;
-  HY_TRY(hyk::ntt_poly_fwd(p, x, x, n, s));
-  HY_TRY(hyk::ntt_poly_inv(p, x, x, n, s));
+  // the forward transform must not run in place: the CTAs of one split transform read every
+  // coefficient of their polynomial (ntt.cuh)
+  u64* tmp = nullptr;
+  HY_CUDA_TRY(cudaMalloc(&tmp, n * p->L * p->N * sizeof(u64)));
+  hy_status st = hyk::ntt_poly_fwd(p, x, tmp, n, s);
+  if (st == HY_OK) st = hyk::ntt_poly_inv(p, tmp, x, n, s);
+  cudaError_t ce = cudaStreamSynchronize(s);
+  cudaFree(tmp);
+  if (st != HY_OK) return st;
+  HY_CHECK(ce == cudaSuccess, HY_ECUDA, "%s", cudaGetErrorString(ce));
   return HY_OK;
 }
 
@@ -621,8 +664,10 @@ extern "C" hy_status hy_rotate(hy_params* p, const uint64_t* ct_in, uint32_t g, 
   HY_CUDA_TRY(cudaSetDevice(p->device));
   cudaStream_t s = (cudaStream_t)stream;
   u64* work = nullptr;
+  GaloisAct act;
+  HY_CHECK(hy_galois_act(g, p->N, &act), HY_EINVAL, "Galois element %u is not odd / < 2N", g);
   HY_CUDA_TRY(cudaMalloc(&work, n * (p->L * p->L + p->L) * p->N * sizeof(u64)));
-  hy_status st = hyk::rotate_ct(p, ct_in, g, it->second.ntt, ct_out, n, work, s);
+  hy_status st = hyk::rotate_ct(p, ct_in, act, it->second.ntt, ct_out, n, work, s);
   cudaError_t ce = cudaStreamSynchronize(s);
   cudaFree(work);
   if (st != HY_OK) return st;

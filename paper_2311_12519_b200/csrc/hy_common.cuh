@@ -63,7 +63,22 @@ struct DevTables {
   u64* psi_rev_sh;
   u64* ipsi_rev;      // psi^{-bitrev(k)}
   u64* ipsi_rev_sh;
+  // [S][B] (B = min(N, HY_NTT_BLOCK), S = N / B): slot-order positions j owned by NTT block h
+  // (ascending) and their butterfly position inside the block.  Slot position j holds the
+  // evaluation at psi^{e_j} (e_j = 3^j for j < N/2, -3^{j-N/2} for j >= N/2, mod 2N), which the
+  // forward transform leaves at butterfly position bitrev((e_j - 1)/2).
+  int32_t* own_j;
+  int32_t* own_k;
 };
+
+// Galois automorphism X -> X^g, g = (+/-) 3^shift mod 2N, acting on slot-ordered NTT vectors:
+// out[j] = in[perm(j)] with perm(j) = ((j + shift) mod N/2) + (half of j, exchanged if swap).
+struct GaloisAct {
+  uint32_t shift;
+  uint32_t swap;
+};
+
+#define HY_NTT_BLOCK 4096  // coefficients per NTT CTA (must match NttCfg in ntt.cuh)
 
 struct KeyEntry {
   uint32_t g;
@@ -84,6 +99,23 @@ struct hy_params {
   u64 keys_version = 0;  // bumped by every hy_keys_upload
 };
 
+bool hy_galois_act(uint32_t g, uint32_t N, GaloisAct* out);
+
+// Row tile of the fused S2+S3 kernel for M MAC rows: -MR = thin kernel with MR <= 2 rows,
+// else WM warps (8 rows each).  Shared by hy_encode_weights (table padding) and the launcher.
+inline int hy_mac_tile(int M) {
+  if (M <= 2) return -M;
+  if (M <= 8) return 1;
+  if (M <= 16) return 2;
+  if (M <= 32) return 4;
+  return 8;
+}
+inline int hy_mac_mpad(int M) {
+  const int t = hy_mac_tile(M);
+  const int bm = t < 0 ? -t : 8 * t;
+  return (M + bm - 1) / bm * bm;
+}  // false if g is not odd / not in Z_2N^*
+
 struct hy_weights {
   hy_params* p;
   hy_conv_shape shape;
@@ -91,21 +123,21 @@ struct hy_weights {
   int M;            // MAC rows per unit
   int K;            // MAC depth per unit (Jc*T dense; T depthwise)
   int wblocks;      // number of distinct weight blocks (1 dense, Jc depthwise)
-  int32_t* d_wm;    // [wblocks][M][K]
+  int Mpad, Kpad;   // M rounded up to the row tile, K rounded up to the MAC chunk
+  double* d_wt;     // [wblocks][Kpad][Mpad] weights (exact small integers), zero padded
   u64* d_sign;      // [L][N] NTT form of the [k,-k] plaintext, then [L][N] Shoup companions
   // workspace (device)
   u64* d_D;         // [U*Jc][L digit][L limb][N] NTT-form digits
   u64* d_C0;        // [U*Jc][L][N]    NTT(c0)
-  u64* d_R;         // [U*Jc][T][2][L][N] rotated inputs (NTT form)
   u64* d_P;         // [U*Jo][cn'][2][L][N] partial sums (NTT form)
   u64* d_D2;        // [U*Jo][L][L][N] digits of P_{g,1}.c1 for the row swap
   u64* d_in;        // staging for hy_conv_eval_host
   u64* d_out;
   u64** d_tap_keys;            // device array of key pointers per tap (nullptr = identity)
-  uint32_t* d_tap_g;           // device array of Galois elements per tap
+  GaloisAct* d_tap_act;        // device array of slot-order automorphism actions per tap
   u64* d_swap_key;
   u64 keys_version;            // params->keys_version the tap table was built from
-  cudaEvent_t ev[5];           // optional stage-boundary events (bench)
+  cudaEvent_t ev[4];           // optional stage-boundary events (bench)
   uint32_t n_ev;
 };
 
@@ -150,12 +182,9 @@ hy_status pointwise_mul(const hy_params* p, const u64* a, const u64* b, u64* c, 
 hy_status shoup_table(const hy_params* p, const u64* w, u64* w_sh, size_t npoly, cudaStream_t s);  // [n][L][N]
 hy_status key_to_ntt(const hy_params* p, const u64* key_coeff, u64* key_ntt, cudaStream_t s);
 hy_status permdecomp(const hy_params* p, const u64* ct, size_t nct, u64* D, u64* C0, cudaStream_t s);
-hy_status permauto(const hy_params* p, const u64* D, const u64* C0, size_t nct, int ntap, u64* const* d_tap_keys,
-                   const uint32_t* h_galois_per_tap, u64* R, cudaStream_t s);
-hy_status mac(const hy_weights* w, size_t nunits, cudaStream_t s);
-hy_status rowswap_digits(const hy_params* p, const u64* Pd, size_t nout, u64* D2, cudaStream_t s);
+hy_status ksmac(const hy_weights* w, size_t nunits, cudaStream_t s);  // fused S2 + S3
 hy_status finish_outputs(const hy_weights* w, size_t nunits, u64* ct_out, cudaStream_t s);
-hy_status rotate_ct(const hy_params* p, const u64* ct_in, uint32_t g, const u64* key, u64* ct_out, size_t n,
+hy_status rotate_ct(const hy_params* p, const u64* ct_in, GaloisAct act, const u64* key, u64* ct_out, size_t n,
                     u64* work, cudaStream_t s);
 hy_status decrypt_phase(const hy_params* p, const u64* s_ntt, const u64* s_ntt_sh, const u64* ct, size_t n,
                         u64* x_out, u64* work, cudaStream_t st);

@@ -167,7 +167,7 @@ struct KSFinishJob {
   const u64* add;
   size_t add_stride;
   const u64* key;
-  uint32_t g;
+  GaloisAct act;
   u64* out;  // [o][2][L][N]
   int L, N, logN;
   LimbConsts lcs;
@@ -178,7 +178,7 @@ struct KSFinishJob {
     limb = b % L;
   }
   __device__ u64 load(int k) const {
-    const int kp = auto_perm(k, g, logN);
+    const int kp = galois_perm(k, act, N >> 1);
     KSSrc src{c0 + (size_t)o * c0_stride, D + (size_t)o * D_stride, diag ? diag + (size_t)o * diag_stride : nullptr};
     u64 r0, r1;
     ks_eval(src, key, L, N, limb, k, kp, lcs.lc[limb], r0, r1);
@@ -269,29 +269,43 @@ struct PhaseInvJob {
 };
 
 template <int LOGN, class Job>
-hy_status launch_fwd_t(const hy_params* p, const Job& job, size_t nblocks, cudaStream_t s) {
-  if (nblocks == 0) return HY_OK;
+hy_status launch_fwd_t(const hy_params* p, const Job& job, size_t npoly, cudaStream_t s) {
+  if (npoly == 0) return HY_OK;
+  using C = NttCfg<LOGN>;
   const size_t sm = ntt_smem_bytes<LOGN>();
   static bool attr_done = false;
   if (!attr_done) {
     HY_CUDA_TRY(cudaFuncSetAttribute(ntt_fwd_kernel<LOGN, Job>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attr_done = true;
   }
-  ntt_fwd_kernel<LOGN, Job><<<(unsigned)nblocks, (1 << LOGN) / 16, sm, s>>>(job, p->tab, limb_consts(p));
+  ntt_fwd_kernel<LOGN, Job><<<(unsigned)(npoly * C::S), C::T, sm, s>>>(job, p->tab, limb_consts(p));
   HY_LAUNCH_CHECK();
   return HY_OK;
 }
 
 template <int LOGN, class Job>
-hy_status launch_inv_t(const hy_params* p, const Job& job, size_t nblocks, cudaStream_t s) {
-  if (nblocks == 0) return HY_OK;
+hy_status launch_inv_t(const hy_params* p, const Job& job, size_t npoly, cudaStream_t s) {
+  if (npoly == 0) return HY_OK;
+  using C = NttCfg<LOGN>;
   const size_t sm = ntt_smem_bytes<LOGN>();
   static bool attr_done = false;
   if (!attr_done) {
     HY_CUDA_TRY(cudaFuncSetAttribute(ntt_inv_kernel<LOGN, Job>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attr_done = true;
   }
-  ntt_inv_kernel<LOGN, Job><<<(unsigned)nblocks, (1 << LOGN) / 16, sm, s>>>(job, p->tab, limb_consts(p));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(npoly * C::S));
+  cfg.blockDim = dim3(C::T);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C::S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HY_CUDA_TRY(cudaLaunchKernelEx(&cfg, ntt_inv_kernel<LOGN, Job>, job, p->tab, limb_consts(p)));
   HY_LAUNCH_CHECK();
   return HY_OK;
 }
@@ -334,57 +348,33 @@ __global__ void shoup_table_kernel(const u64* __restrict__ w, u64* __restrict__ 
   }
 }
 
-// S2 PermAuto, materialised: R[ct][tap][2][L][N] (tap without key = identity: (C0, D_ll)).
-__global__ void __launch_bounds__(256) permauto_kernel(const u64* __restrict__ D, const u64* __restrict__ C0, int nct,
-                                                       int T, const u64* const* __restrict__ tap_keys,
-                                                       const uint32_t* __restrict__ tap_g, u64* __restrict__ R, int L,
-                                                       int logN, LimbConsts lcs) {
-  const int N = 1 << logN;
-  const size_t total = (size_t)nct * T * L * N;
-  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (size_t)gridDim.x * blockDim.x) {
-    const int k = (int)(idx & (N - 1));
-    size_t rest = idx >> logN;
-    const int l = (int)(rest % L);
-    rest /= L;
-    const int tap = (int)(rest % T);
-    const int c = (int)(rest / T);
-    const u64* key = tap_keys[tap];
-    u64 r0, r1;
-    if (key == nullptr) {
-      r0 = C0[((size_t)c * L + l) * N + k];
-      r1 = D[(((size_t)c * L + l) * L + l) * N + k];
-    } else {
-      const int kp = auto_perm(k, tap_g[tap], logN);
-      KSSrc src{C0 + (size_t)c * L * N, D + (size_t)c * L * L * N, nullptr};
-      ks_eval(src, key, L, N, l, k, kp, lcs.lc[l], r0, r1);
-      r0 = csub(r0, lcs.lc[l].q);
-      r1 = csub(r1, lcs.lc[l].q);
-    }
-    u64* out = R + ((size_t)(c * T + tap) * 2 * L + l) * N + k;
-    out[0] = r0;
-    out[(size_t)L * N] = r1;
-  }
-}
-
 // ------------------------------------------------------------------------------------------
-// S3: lazy MAC + WHT + one reduction + sign PMult
+// S2 + S3 fused: hoisted PermAuto computed on the fly, lazy MAC of the int weights, Walsh-
+// Hadamard butterflies on the accumulators, ONE reduction per output coefficient, PMult by the
+// sign plaintext, HAdd (Algorithm :1536-1551 [ign]).
 //
-// Exact integer accumulation on the FP64 pipe: each R coefficient x < 2^60 is split into
-// 30-bit halves (exact doubles); products with |w| <= 128 are < 2^37 and sums of up to
-// 2^16 of them stay < 2^53, so every DFMA is exact.  One reduction per output coefficient.
+// Rotated input R_{c,tau} (never materialised in HBM), for limb l and slot-order position j:
+//   R.c0[j] = C0_c[perm(j)] + sum_i D_{c,i}[perm(j)] b_{tau,i}[j],  R.c1[j] = sum_i D_{c,i}[perm(j)] a_{tau,i}[j]
+// (identity tap: R = (C0_c, D_{c,l,l})).  perm = cyclic shift (+ half swap) in slot order.
+//
+// MAC exactness: every canonical R value x < 2^60 is split into 30-bit halves,
+// exact as doubles; |w| <= 128 so each product is < 2^37 and sums of up to 2^16 terms stay below
+// 2^53: every DFMA is exact, accumulation order is irrelevant, and one reduction per output
+// coefficient recovers the residue (lazy reduction).
 // ------------------------------------------------------------------------------------------
-struct MacArgs {
-  const u64* R;       // [units][K][ncols]
-  const int32_t* wm;  // [wblocks][Mpad][K]
-  u64* out;           // CN=1: [units][M][ncols]; CN=2: [units][M/2][ncols]
-  const u64* sign;    // [L][N], then [L][N] Shoup
-  int K, M, Mpad, ncols, wblocks, L, logN, kscale;
+struct KsMacArgs {
+  const u64* D;                // [J][L digit][L limb][N] slot-order NTT
+  const u64* C0;               // [J][L][N]
+  u64* const* keys;            // [T] key per tap (nullptr = identity)
+  const GaloisAct* act;        // [T]
+  const double* wt;            // [wblocks][Kpad][Mpad]
+  u64* out;                    // [z][M'][2][L][N], M' = M (cn 1) or M/2 (cn 2)
+  const u64* sign;             // [L][N] sign plaintext (NTT), then [L][N] Shoup companions
+  int T, Jcb, K, Kpad, M, Mpad, wblocks, L, logN, kscale, cn;
   LimbConsts lcs;
 };
 
-constexpr int MAC_THREADS = 128;
-constexpr int MAC_KC = 32;
+constexpr uint32_t M30 = 0x3FFFFFFFu;
 
 __device__ __forceinline__ u64 reduce_wide(long long H, long long Lo, const LimbConst& c) {
   // value H * 2^30 + Lo (|H|, |Lo| < 2^59) mod q, canonical
@@ -396,79 +386,301 @@ __device__ __forceinline__ u64 reduce_wide(long long H, long long Lo, const Limb
   return csub(s, c.q);
 }
 
-template <int TM, int CN>
-__global__ void __launch_bounds__(MAC_THREADS) mac_kernel(MacArgs a) {
-  __shared__ double sw[MAC_KC][TM];
-  const int col = blockIdx.x * MAC_THREADS + threadIdx.x;
-  const int row0 = blockIdx.y * TM;
-  const int unit = blockIdx.z;
-  const int wb = unit % a.wblocks;
-  const u64* __restrict__ Rp = a.R + (size_t)unit * a.K * a.ncols + col;
-  const int32_t* __restrict__ W = a.wm + ((size_t)wb * a.Mpad + row0) * a.K;
-  double acc_h[TM], acc_l[TM];
+// Key words of tap t for limb l at slot position j: digit i, component comp at
+// key[((2i + comp) L + l) N + j], Shoup companion one key block (2 L L N words) later.
+// Held per thread in registers (KeyRegs) while consecutive K terms use the same tap: the K axis
+// is ordered tap-major (kk = tau * Jcb + c), so a thread reloads them once per tap.
+template <int LT>
+struct KeyRegs {
+  static constexpr int NL = LT > 0 ? LT : 1;
+  u64 v[2 * NL], sh[2 * NL];
+  int tau = -1;
+  __device__ __forceinline__ void load(const u64* __restrict__ key, int logN, int l, int j) {
+    const size_t N = (size_t)1 << logN, LN = (size_t)LT * N, kblk = 2 * LT * LN;
+    const u64* kb = key + (size_t)l * N + j;
 #pragma unroll
-  for (int r = 0; r < TM; r++) acc_h[r] = acc_l[r] = 0.0;
-
-  for (int kc0 = 0; kc0 < a.K; kc0 += MAC_KC) {
-    const int kcn = min(MAC_KC, a.K - kc0);
-    __syncthreads();
-    for (int e = threadIdx.x; e < MAC_KC * TM; e += MAC_THREADS) {
-      const int kk = e / TM, r = e % TM;
-      sw[kk][r] = (kk < kcn) ? (double)W[(size_t)r * a.K + kc0 + kk] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int kk = 0; kk < kcn; kk++) {
-      const u64 x = __ldg(Rp + (size_t)(kc0 + kk) * a.ncols);
-      const double xh = (double)(uint32_t)(x >> 30);
-      const double xl = (double)(uint32_t)(x & 0x3FFFFFFFull);
-#pragma unroll
-      for (int r = 0; r < TM; r++) {
-        const double w = sw[kk][r];
-        acc_h[r] = fma(w, xh, acc_h[r]);
-        acc_l[r] = fma(w, xl, acc_l[r]);
-      }
+    for (int x = 0; x < 2 * LT; x++) {
+      v[x] = __ldg(kb + x * LN);
+      sh[x] = __ldg(kb + x * LN + kblk);
     }
   }
+};
 
+// key-switched pair (R.c0, R.c1) of one input ct at limb l, reading slot position jp
+template <int LT>
+__device__ __forceinline__ void ks_pair_regs(const u64* __restrict__ D, const u64* __restrict__ C0,
+                                             const KeyRegs<LT>& k, int logN, int l, int jp, const LimbConst& c,
+                                             u64& r0, u64& r1) {
+  const size_t N = (size_t)1 << logN;
+  const u64 q = c.q, q2 = c.two_q;
+  u64 dv[LT];
+#pragma unroll
+  for (int i = 0; i < LT; i++) dv[i] = __ldg(D + ((size_t)i * LT + l) * N + jp);
+  u64 a0 = __ldg(C0 + (size_t)l * N + jp), a1 = 0;
+#pragma unroll
+  for (int i = 0; i < LT; i++) {
+    a0 = csub(a0 + shoup_mul(dv[i], k.v[2 * i], k.sh[2 * i], q), q2);
+    a1 = csub(a1 + shoup_mul(dv[i], k.v[2 * i + 1], k.sh[2 * i + 1], q), q2);
+  }
+  r0 = csub(a0, q);
+  r1 = csub(a1, q);
+}
+
+// generic (runtime L) version reading the key from global memory
+__device__ __forceinline__ void ks_pair_any(const u64* __restrict__ D, const u64* __restrict__ C0,
+                                            const u64* __restrict__ key, int L, int logN, int l, int j, int jp,
+                                            const LimbConst& c, u64& r0, u64& r1) {
+  const size_t N = (size_t)1 << logN;
+  const size_t LN = (size_t)L * N, kblk = 2 * L * LN;
+  const u64 q = c.q, q2 = c.two_q;
+  u64 a0 = __ldg(C0 + (size_t)l * N + jp), a1 = 0;
+  const u64* kb = key + (size_t)l * N + j;
+  for (int i = 0; i < L; i++) {
+    const u64 dv = __ldg(D + ((size_t)i * L + l) * N + jp);
+    const u64* k0 = kb + (size_t)(2 * i) * LN;
+    const u64* k1 = k0 + LN;
+    a0 = csub(a0 + shoup_mul(dv, __ldg(k0), __ldg(k0 + kblk), q), q2);
+    a1 = csub(a1 + shoup_mul(dv, __ldg(k1), __ldg(k1 + kblk), q), q2);
+  }
+  r0 = csub(a0, q);
+  r1 = csub(a1, q);
+}
+
+// R value pair of K term kk (= tau * Jcb + c) of unit block z at (l, j)
+template <int LT>
+__device__ __forceinline__ void r_value(const KsMacArgs& a, const u64* const* keys, const GaloisAct* act, int z,
+                                        int kk, int l, int j, const LimbConst& c, KeyRegs<LT>& kr, u64& r0,
+                                        u64& r1) {
+  const int L = LT > 0 ? LT : a.L;
   const int N = 1 << a.logN;
-  const int l = (col >> a.logN) % a.L;
-  const int kidx = col & (N - 1);
-  const LimbConst& c = a.lcs.lc[l];
-  if (CN == 1) {
-#pragma unroll
-    for (int r = 0; r < TM; r++) {
-      if (row0 + r < a.M)
-        a.out[((size_t)unit * a.M + row0 + r) * a.ncols + col] =
-            reduce_wide(__double2ll_rn(acc_h[r]), __double2ll_rn(acc_l[r]), c);
+  const size_t LN = (size_t)L * N;
+  const int t = kk / a.Jcb, cc = kk - t * a.Jcb;
+  const size_t ct = (size_t)z * a.Jcb + cc;
+  const u64* C0 = a.C0 + ct * LN;
+  const u64* D = a.D + ct * L * LN;
+  const u64* key = keys[t];
+  if (key == nullptr) {
+    r0 = __ldg(C0 + (size_t)l * N + j);
+    r1 = __ldg(D + ((size_t)l * L + l) * N + j);
+    return;
+  }
+  const int jp = galois_perm(j, act[t], N >> 1);
+  if constexpr (LT > 0) {
+    if (kr.tau != t) {
+      kr.load(key, a.logN, l, j);
+      kr.tau = t;
     }
+    ks_pair_regs<LT>(D, C0, kr, a.logN, l, jp, c, r0, r1);
   } else {
-    const u64 sg = a.sign[(size_t)l * N + kidx];
-    const u64 sgs = a.sign[(size_t)(a.L + l) * N + kidx];
+    ks_pair_any(D, C0, key, L, a.logN, l, j, jp, c, r0, r1);
+  }
+}
+
+__device__ __forceinline__ void store_outputs(const KsMacArgs& a, int z, int row, int comp, int l, int j,
+                                              const double* ah, const double* al, int nrows) {
+  // rows row .. row+nrows-1 (nrows even for cn = 2) of unit block z at (comp, l, j)
+  const int N = 1 << a.logN;
+  const size_t LN = (size_t)a.L * N;
+  const LimbConst& c = a.lcs.lc[l];
+  if (a.cn == 1) {
+    for (int r = 0; r < nrows; r++)
+      if (row + r < a.M)
+        a.out[((size_t)(z * a.M + row + r) * 2 + comp) * LN + (size_t)l * N + j] =
+            reduce_wide(__double2ll_rn(ah[r]), __double2ll_rn(al[r]), c);
+  } else {
+    const u64 sg = __ldg(a.sign + (size_t)l * N + j), sgs = __ldg(a.sign + LN + (size_t)l * N + j);
     const long long kk = a.kscale;
-#pragma unroll
-    for (int r = 0; r < TM; r += 2) {
-      if (row0 + r < a.M) {
-        const long long H0 = __double2ll_rn(acc_h[r]), L0 = __double2ll_rn(acc_l[r]);
-        const long long H1 = __double2ll_rn(acc_h[r + 1]), L1 = __double2ll_rn(acc_l[r + 1]);
+    for (int r = 0; r < nrows; r += 2) {
+      if (row + r < a.M) {
+        const long long H0 = __double2ll_rn(ah[r]), L0 = __double2ll_rn(al[r]);
+        const long long H1 = __double2ll_rn(ah[r + 1]), L1 = __double2ll_rn(al[r + 1]);
         // Walsh-Hadamard on the accumulators (Eq. 2): A0 = k (B0 + B1), A1 = B0 - B1
         const u64 a0 = reduce_wide(kk * (H0 + H1), kk * (L0 + L1), c);
         const u64 a1 = reduce_wide(H0 - H1, L0 - L1, c);
         // PMult by the [k, -k] plaintext (NTT form, Shoup) and HAdd
         u64 v = a0 + shoup_mul(a1, sg, sgs, c.q);
         v = csub(csub(v, c.two_q), c.q);
-        a.out[((size_t)unit * (a.M / 2) + (row0 + r) / 2) * a.ncols + col] = v;
+        a.out[((size_t)(z * (a.M / 2) + (row + r) / 2) * 2 + comp) * LN + (size_t)l * N + j] = v;
       }
     }
   }
 }
 
-template <int TM, int CN>
-hy_status launch_mac_t(const MacArgs& a, int units, cudaStream_t s) {
-  dim3 grid(a.ncols / MAC_THREADS, a.Mpad / TM, units);
-  mac_kernel<TM, CN><<<grid, MAC_THREADS, 0, s>>>(a);
+// ---- GEMM-shaped variant: C[M][2 x BNP] += W[M][K] x R[K][2 x BNP], K chunked by KC = 2 WM.
+// 256 threads = WM row-group warps x PG = 8 / WM position groups; warp (rg, pg) owns rows
+// 8 rg .. 8 rg + 7 of the row tile, lane owns position 32 pg + lane (both components).  Every
+// thread first produces 2 R items of the next chunk into shared memory (double-buffered), then
+// runs its 8 x 2 x 2 DFMAs per k.  <= 128 registers so that two CTAs share an SM: one CTA's
+// key switching (INT pipes, L2 loads) overlaps the other's DFMAs.
+template <int WM, int LT>
+__global__ void __launch_bounds__(256, 2) ksmac_gemm_kernel(KsMacArgs a) {
+  constexpr int BM = 8 * WM, PG = 8 / WM, BNP = 32 * PG, KC = 2 * WM;
+  static_assert(KC * BNP == 512, "two R items per thread per chunk");
+  extern __shared__ __align__(16) unsigned char smraw[];
+  auto Rs = reinterpret_cast<double2(*)[KC][2][BNP]>(smraw);                                // [2][KC][2][BNP]
+  auto Ws = reinterpret_cast<double(*)[KC][BM]>(smraw + sizeof(double2) * 2 * KC * 2 * BNP);  // [2][KC][BM]
+  __shared__ const u64* s_key[HY_MAX_TAPS];
+  __shared__ GaloisAct s_act[HY_MAX_TAPS];
+
+  const int N = 1 << a.logN;
+  const int tiles = N / BNP;
+  const int l = blockIdx.x / tiles, j0 = (blockIdx.x % tiles) * BNP;
+  const int row0 = blockIdx.y * BM, z = blockIdx.z;
+  const double* __restrict__ wt = a.wt + (size_t)(z % a.wblocks) * a.Kpad * a.Mpad;
+  const LimbConst cst = a.lcs.lc[l];
+  for (int t = threadIdx.x; t < a.T; t += 256) {
+    s_key[t] = a.keys[t];
+    s_act[t] = a.act[t];
+  }
+  __syncthreads();
+
+  // Every thread produces the items (kkl, p) = (tid / BNP + 256 h / BNP, tid % BNP), h = 0, 1:
+  // always the same position p, so the tap keys stay in registers across items and chunks.
+  constexpr int WPT = (KC * BM + 255) / 256;  // weights staged per thread per chunk
+  KeyRegs<LT> kr;
+  auto produce = [&](int chunk, int buf) {
+    double wv[WPT];
+#pragma unroll
+    for (int u = 0; u < WPT; u++) {
+      const int it = threadIdx.x + 256 * u;
+      if (it < KC * BM) wv[u] = __ldg(wt + (size_t)(chunk * KC + it / BM) * a.Mpad + row0 + it % BM);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int it = threadIdx.x + 256 * h;
+      const int kkl = it / BNP, p = it % BNP, kk = chunk * KC + kkl;
+      u64 r0 = 0, r1 = 0;
+      if (kk < a.K) r_value<LT>(a, s_key, s_act, z, kk, l, j0 + p, cst, kr, r0, r1);
+      Rs[buf][kkl][0][p] = make_double2((double)(uint32_t)(r0 >> 30), (double)(uint32_t)(r0 & M30));
+      Rs[buf][kkl][1][p] = make_double2((double)(uint32_t)(r1 >> 30), (double)(uint32_t)(r1 & M30));
+    }
+#pragma unroll
+    for (int u = 0; u < WPT; u++) {
+      const int it = threadIdx.x + 256 * u;
+      if (it < KC * BM) Ws[buf][it / BM][it % BM] = wv[u];
+    }
+  };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rg = warp % WM, pg = warp / WM;
+  const int pos = pg * 32 + lane;
+  double acc_h[8][2], acc_l[8][2];
+#pragma unroll
+  for (int r = 0; r < 8; r++)
+#pragma unroll
+    for (int n = 0; n < 2; n++) acc_h[r][n] = acc_l[r][n] = 0.0;
+
+  const int nchunks = a.Kpad / KC;
+  produce(0, 0);
+  __syncthreads();
+  for (int ch = 0; ch < nchunks; ch++) {
+    const int buf = ch & 1;
+    if (ch + 1 < nchunks) produce(ch + 1, buf ^ 1);
+#pragma unroll
+    for (int kkl = 0; kkl < KC; kkl++) {
+      const double2* wp = reinterpret_cast<const double2*>(&Ws[buf][kkl][rg * 8]);
+      double w[8];
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const double2 t2 = wp[r];
+        w[2 * r] = t2.x;
+        w[2 * r + 1] = t2.y;
+      }
+      const double2 x0 = Rs[buf][kkl][0][pos], x1 = Rs[buf][kkl][1][pos];
+#pragma unroll
+      for (int r = 0; r < 8; r++) {
+        acc_h[r][0] = fma(w[r], x0.x, acc_h[r][0]);
+        acc_l[r][0] = fma(w[r], x0.y, acc_l[r][0]);
+        acc_h[r][1] = fma(w[r], x1.x, acc_h[r][1]);
+        acc_l[r][1] = fma(w[r], x1.y, acc_l[r][1]);
+      }
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int n = 0; n < 2; n++) {
+    double ah[8], al[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      ah[r] = acc_h[r][n];
+      al[r] = acc_l[r][n];
+    }
+    store_outputs(a, z, row0 + rg * 8, n, l, j0 + pos, ah, al, 8);
+  }
+}
+
+// ---- thin variant (M <= 2 rows: depthwise): one thread per (limb, position), all K terms in
+// registers, no shared memory.
+template <int MR, int LT>
+__global__ void __launch_bounds__(256) ksmac_thin_kernel(KsMacArgs a) {
+  const int N = 1 << a.logN;
+  const int idx = blockIdx.x * 256 + threadIdx.x;
+  const int l = idx >> a.logN, j = idx & (N - 1);
+  if (l >= a.L) return;
+  const int z = blockIdx.z;
+  const double* __restrict__ wt = a.wt + (size_t)(z % a.wblocks) * a.Kpad * a.Mpad;
+  const LimbConst cst = a.lcs.lc[l];
+  double ah[2][MR], al[2][MR];
+#pragma unroll
+  for (int c = 0; c < 2; c++)
+#pragma unroll
+    for (int r = 0; r < MR; r++) ah[c][r] = al[c][r] = 0.0;
+  KeyRegs<LT> kr;
+  for (int kk = 0; kk < a.K; kk++) {
+    u64 r0, r1;
+    r_value<LT>(a, a.keys, a.act, z, kk, l, j, cst, kr, r0, r1);
+    const double x0h = (double)(uint32_t)(r0 >> 30), x0l = (double)(uint32_t)(r0 & M30);
+    const double x1h = (double)(uint32_t)(r1 >> 30), x1l = (double)(uint32_t)(r1 & M30);
+#pragma unroll
+    for (int r = 0; r < MR; r++) {
+      const double w = __ldg(wt + (size_t)kk * a.Mpad + r);
+      ah[0][r] = fma(w, x0h, ah[0][r]);
+      al[0][r] = fma(w, x0l, al[0][r]);
+      ah[1][r] = fma(w, x1h, ah[1][r]);
+      al[1][r] = fma(w, x1l, al[1][r]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 2; c++) store_outputs(a, z, 0, c, l, j, ah[c], al[c], MR);
+}
+
+template <int WM, int LT>
+hy_status launch_ksmac_gemm(const KsMacArgs& a, int units, cudaStream_t s) {
+  const int N = 1 << a.logN, BNP = 256 / WM, KC = 2 * WM;
+  const size_t sm = sizeof(double2) * 2 * KC * 2 * BNP + sizeof(double) * 2 * KC * 8 * WM;
+  static bool attr_done = false;
+  if (!attr_done) {
+    HY_CUDA_TRY(cudaFuncSetAttribute(ksmac_gemm_kernel<WM, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    attr_done = true;
+  }
+  dim3 grid((unsigned)(a.L * (N / BNP)), (unsigned)(a.Mpad / (8 * WM)), (unsigned)units);
+  ksmac_gemm_kernel<WM, LT><<<grid, 256, sm, s>>>(a);
   HY_LAUNCH_CHECK();
   return HY_OK;
+}
+
+template <int MR, int LT>
+hy_status launch_ksmac_thin(const KsMacArgs& a, int units, cudaStream_t s) {
+  const int N = 1 << a.logN;
+  dim3 grid((unsigned)((a.L * N + 255) / 256), 1, (unsigned)units);
+  ksmac_thin_kernel<MR, LT><<<grid, 256, 0, s>>>(a);
+  HY_LAUNCH_CHECK();
+  return HY_OK;
+}
+
+template <int LT>
+hy_status launch_ksmac(const KsMacArgs& a, int tile, int units, cudaStream_t s) {
+  switch (tile) {
+    case -1: return launch_ksmac_thin<1, LT>(a, units, s);
+    case -2: return launch_ksmac_thin<2, LT>(a, units, s);
+    case 1: return launch_ksmac_gemm<1, LT>(a, units, s);
+    case 2: return launch_ksmac_gemm<2, LT>(a, units, s);
+    case 4: return launch_ksmac_gemm<4, LT>(a, units, s);
+    case 8: return launch_ksmac_gemm<8, LT>(a, units, s);
+  }
+  hy_set_error("ksmac: bad row tile");
+  return HY_EINVAL;
 }
 
 }  // namespace
@@ -513,55 +725,37 @@ hy_status permdecomp(const hy_params* p, const u64* ct, size_t nct, u64* D, u64*
   return launch_fwd(p, j, nct * (p->L * p->L + p->L), s);
 }
 
-hy_status permauto(const hy_params* p, const u64* D, const u64* C0, size_t nct, int ntap, u64* const* d_tap_keys,
-                   const uint32_t* d_tap_g, u64* R, cudaStream_t s) {
-  const size_t total = nct * ntap * p->L * p->N;
-  if (!total) return HY_OK;
-  const unsigned blocks = (unsigned)std::min<size_t>((total + 255) / 256, 148 * 64);
-  permauto_kernel<<<blocks, 256, 0, s>>>(D, C0, (int)nct, ntap, d_tap_keys, d_tap_g, R, (int)p->L, (int)p->logN,
-                                         limb_consts(p));
-  HY_LAUNCH_CHECK();
-  return HY_OK;
-}
-
-hy_status mac(const hy_weights* w, size_t nunits, cudaStream_t s) {
+hy_status ksmac(const hy_weights* w, size_t nunits, cudaStream_t s) {
   const hy_params* p = w->p;
   const hy_layout& lay = w->lay;
-  MacArgs a;
-  a.R = w->d_R;
-  a.wm = w->d_wm;
+  const bool dw = w->shape.depthwise != 0;
+  KsMacArgs a;
+  a.D = w->d_D;
+  a.C0 = w->d_C0;
+  a.keys = w->d_tap_keys;
+  a.act = w->d_tap_act;
+  a.wt = w->d_wt;
   a.out = w->d_P;
   a.sign = w->d_sign;
+  a.T = (int)lay.n_taps;
+  a.Jcb = dw ? 1 : (int)lay.Jc;
   a.K = w->K;
+  a.Kpad = w->Kpad;
   a.M = w->M;
-  a.ncols = 2 * p->L * p->N;
+  a.Mpad = w->Mpad;
   a.wblocks = w->wblocks;
-  a.L = p->L;
-  a.logN = p->logN;
+  a.L = (int)p->L;
+  a.logN = (int)p->logN;
   a.kscale = (int)lay.k;
+  a.cn = (int)lay.cn;
   a.lcs = limb_consts(p);
-  const bool dw = w->shape.depthwise != 0;
   const int units = (int)(dw ? nunits * lay.Jc : nunits);
-  const int tm = w->M >= 16 ? 16 : (w->M >= 8 ? 8 : (w->M >= 4 ? 4 : (w->M >= 2 ? 2 : 1)));
-  a.Mpad = (w->M + tm - 1) / tm * tm;
-  if (lay.cn == 2) {
-    switch (tm) {
-      case 16: return launch_mac_t<16, 2>(a, units, s);
-      case 8: return launch_mac_t<8, 2>(a, units, s);
-      case 4: return launch_mac_t<4, 2>(a, units, s);
-      case 2: return launch_mac_t<2, 2>(a, units, s);
-    }
-  } else {
-    switch (tm) {
-      case 16: return launch_mac_t<16, 1>(a, units, s);
-      case 8: return launch_mac_t<8, 1>(a, units, s);
-      case 4: return launch_mac_t<4, 1>(a, units, s);
-      case 2: return launch_mac_t<2, 1>(a, units, s);
-      case 1: return launch_mac_t<1, 1>(a, units, s);
-    }
+  const int tile = hy_mac_tile(w->M);
+  switch (p->L) {  // key switching with a compile-time digit count for the common L
+    case 2: return launch_ksmac<2>(a, tile, units, s);
+    case 3: return launch_ksmac<3>(a, tile, units, s);
+    default: return launch_ksmac<0>(a, tile, units, s);
   }
-  hy_set_error("mac: bad row tile");
-  return HY_EINVAL;
 }
 
 hy_status finish_outputs(const hy_weights* w, size_t nunits, u64* ct_out, cudaStream_t s) {
@@ -590,7 +784,7 @@ hy_status finish_outputs(const hy_weights* w, size_t nunits, u64* ct_out, cudaSt
     jc.add = w->d_P;  // P_{g,0}
     jc.add_stride = 2 * ct_words;
     jc.key = w->d_swap_key;
-    jc.g = 2 * p->N - 1;
+    jc.act = GaloisAct{0u, 1u};  // X -> X^{2N-1}: exchange the two slot rows
     jc.out = ct_out;
     jc.L = (int)L;
     jc.N = (int)N;
@@ -602,7 +796,7 @@ hy_status finish_outputs(const hy_weights* w, size_t nunits, u64* ct_out, cudaSt
   return launch_inv(p, j, nout * 2 * L, s);
 }
 
-hy_status rotate_ct(const hy_params* p, const u64* ct_in, uint32_t g, const u64* key, u64* ct_out, size_t n,
+hy_status rotate_ct(const hy_params* p, const u64* ct_in, GaloisAct act, const u64* key, u64* ct_out, size_t n,
                     u64* work, cudaStream_t s) {
   const size_t L = p->L, N = p->N;
   u64* D = work;
@@ -618,7 +812,7 @@ hy_status rotate_ct(const hy_params* p, const u64* ct_in, uint32_t g, const u64*
   j.add = nullptr;
   j.add_stride = 0;
   j.key = key;
-  j.g = g;
+  j.act = act;
   j.out = ct_out;
   j.L = (int)L;
   j.N = (int)N;

@@ -12,11 +12,18 @@
 //            followed by the N^{-1} scaling.
 // Between groups the coefficients are exchanged through shared memory padded by one word
 // per 16 (index k -> k + k/16) so the small-span groups are bank-conflict free.
-// Output slot k of the forward transform holds a(psi^{2 bitrev(k) + 1}).
+// Butterfly position k of the forward transform holds a(psi^{2 bitrev(k) + 1}); the kernels
+// store (and the inverse loads) in SLOT ORDER instead: global position j holds the evaluation
+// at psi^{e_j}, e_j = 3^j (j < N/2) or -3^{j-N/2} (j >= N/2) mod 2N, through the table
+// k_of_slot (the permutation is applied between shared memory and HBM, so it is free).  In slot
+// order every Galois automorphism X -> X^{(+/-)3^s} is a cyclic shift by s inside each half,
+// plus a half exchange for the minus sign — PermAuto reads become streams.
 //
 // Twiddles: psi_rev[m + i] = psi^{bitrev(m + i)} with Shoup companions (per limb tables).
 // Butterflies keep Harvey's lazy ranges: forward values in [0, 4q), inverse in [0, 2q).
 #pragma once
+
+#include <cooperative_groups.h>
 
 #include "hy_common.cuh"
 
@@ -43,184 +50,270 @@ __device__ __forceinline__ void gs_bfly(u64& x, u64& y, u64 w, u64 wsh, u64 q2) 
 }
 
 // ---------------------------------------------------------------------------------------
-// forward transform; Job: bind(block) sets `limb`; load(k) returns a value in [0, 4q);
-// store(k, v) receives canonical v in [0, q).
+// Kernel geometry.  A transform of N = S * B coefficients runs on S CTAs of T = B / 8 threads
+// (B = min(N, 4096), 8 values per thread, radix-8 register groups between shared-memory
+// exchanges).  Forward (Cooley-Tukey, natural in): after its first log2(S) stages the array
+// splits into S independent blocks, so CTA h recomputes those stages for block h only from the S
+// inputs x[r + h'B] (one extra Shoup product per value at S = 2) and then transforms its block
+// alone.  Inverse (Gentleman-Sande, slot order in): CTA h transforms block h, then the S CTAs of
+// a thread-block cluster exchange through distributed shared memory for the last log2(S)
+// stages.  Splitting halves (S = 2) the single-transform latency at N = 8192 and keeps every
+// CTA at 512 threads x <= 64 registers (3 CTAs / SM by registers).
+// ---------------------------------------------------------------------------------------
+template <int LOGN>
+struct NttCfg {
+  static constexpr int LOGS = LOGN > 12 ? LOGN - 12 : 0;
+  static constexpr int S = 1 << LOGS;
+  static constexpr int LOGB = LOGN - LOGS;
+  static constexpr int B = 1 << LOGB;
+  static constexpr int LOGV = 3;
+  static constexpr int V = 1 << LOGV;
+  static constexpr int T = B / V;
+  static constexpr int FULL = LOGB / LOGV;
+  static constexpr int REM = LOGB % LOGV;
+};
+
+// ---------------------------------------------------------------------------------------
+// forward transform; Job: bind(poly) sets `limb`; load(k) (coefficient k) returns a value in
+// [0, 4q); store(j, v) receives canonical v in [0, q) for slot-order position j.
+// tab.own_j / own_k: slot positions owned by block h (ascending) and their in-block butterfly
+// position, [S][B] each.
 // ---------------------------------------------------------------------------------------
 template <int LOGN, class Job>
-__global__ void __launch_bounds__((1 << LOGN) / 16) ntt_fwd_kernel(Job job, DevTables tab, LimbConsts L) {
-  constexpr int N = 1 << LOGN;
-  constexpr int T = N / 16;
-  constexpr int FULL = LOGN / 4;
-  constexpr int REM = LOGN % 4;
+__global__ void __launch_bounds__(NttCfg<LOGN>::T) ntt_fwd_kernel(Job job, DevTables tab, LimbConsts L) {
+  using C = NttCfg<LOGN>;
+  constexpr int S = C::S, B = C::B, V = C::V, T = C::T;
   extern __shared__ u64 sm[];
   const int tid = threadIdx.x;
+  const int h = blockIdx.x % S;
   Job jb = job;
-  jb.bind(blockIdx.x);
+  jb.bind(blockIdx.x / S);
   const int l = jb.limb;
   const u64 q = L.lc[l].q, q2 = L.lc[l].two_q;
-  const u64* __restrict__ W = tab.psi_rev + (size_t)l * N;
-  const u64* __restrict__ Ws = tab.psi_rev_sh + (size_t)l * N;
-  u64 v[16];
+  const u64* __restrict__ W = tab.psi_rev + ((size_t)l << LOGN);
+  const u64* __restrict__ Ws = tab.psi_rev_sh + ((size_t)l << LOGN);
+  u64 v[V];
 #pragma unroll
-  for (int r = 0; r < 16; r++) v[r] = jb.load(tid + r * T);
-
-  int thi = N / 2;
+  for (int r = 0; r < V; r++) {
+    const int rr = tid + r * T;
+    if constexpr (S == 1) {
+      v[r] = jb.load(rr);
+    } else {
+      u64 y[S];
 #pragma unroll
-  for (int gi = 0; gi < FULL; gi++) {
-    const int delta = thi >> 3;
-    const int base = (tid / delta) * (16 * delta) + (tid % delta);
+      for (int g = 0; g < S; g++) y[g] = jb.load(rr + g * B);
+#pragma unroll
+      for (int st = 0; st < C::LOGS; st++) {
+        const int m = 1 << st, span = S / (2 * m);
+#pragma unroll
+        for (int g = 0; g < S; g++)
+          if ((g & span) == 0) {
+            const int widx = m + g / (2 * span);
+            ct_bfly(y[g], y[g + span], __ldg(W + widx), __ldg(Ws + widx), q, q2);
+          }
+      }
+      v[r] = y[0];
+#pragma unroll
+      for (int g = 1; g < S; g++)
+        if (g == h) v[r] = y[g];
+    }
+  }
+  // local stages: global stage with m = S m_loc blocks uses twiddle m_loc (S + h) + i_loc
+  int thi = B / 2;
+#pragma unroll
+  for (int gi = 0; gi < C::FULL; gi++) {
+    const int delta = thi >> (C::LOGV - 1);
+    const int base = (tid / delta) * (V * delta) + (tid % delta);
     if (gi > 0) {
 #pragma unroll
-      for (int r = 0; r < 16; r++) v[r] = sm[smem_pad(base + r * delta)];
+      for (int r = 0; r < V; r++) v[r] = sm[smem_pad(base + r * delta)];
     }
 #pragma unroll
-    for (int s = 0; s < 4; s++) {
+    for (int s = 0; s < C::LOGV; s++) {
       const int t = thi >> s;
-      const int step = 8 >> s;
-      const int m = N / (2 * t);
+      const int step = (V / 2) >> s;
+      const int mloc = B / (2 * t);
 #pragma unroll
-      for (int r = 0; r < 16; r++) {
+      for (int r = 0; r < V; r++) {
         if ((r & step) == 0) {
           const int j = base + r * delta;
-          const int widx = m + j / (2 * t);
+          const int widx = mloc * (S + h) + j / (2 * t);
           ct_bfly(v[r], v[r + step], __ldg(W + widx), __ldg(Ws + widx), q, q2);
         }
       }
     }
 #pragma unroll
-    for (int r = 0; r < 16; r++) sm[smem_pad(base + r * delta)] = v[r];
+    for (int r = 0; r < V; r++) sm[smem_pad(base + r * delta)] = v[r];
     __syncthreads();
-    thi >>= 4;
+    thi >>= C::LOGV;
   }
-  if constexpr (REM > 0) {
-    // spans 2^{REM-1} .. 1 over 16 consecutive coefficients per thread
-    const int base = 16 * tid;
+  if constexpr (C::REM > 0) {
+    const int base = V * tid;
 #pragma unroll
-    for (int r = 0; r < 16; r++) v[r] = sm[smem_pad(base + r)];
+    for (int r = 0; r < V; r++) v[r] = sm[smem_pad(base + r)];
 #pragma unroll
-    for (int s = 0; s < REM; s++) {
-      const int t = (1 << (REM - 1)) >> s;
-      const int m = N / (2 * t);
+    for (int s = 0; s < C::REM; s++) {
+      const int t = (1 << (C::REM - 1)) >> s;
+      const int mloc = B / (2 * t);
 #pragma unroll
-      for (int r = 0; r < 16; r++) {
+      for (int r = 0; r < V; r++) {
         if ((r & t) == 0) {
           const int j = base + r;
-          const int widx = m + j / (2 * t);
+          const int widx = mloc * (S + h) + j / (2 * t);
           ct_bfly(v[r], v[r + t], __ldg(W + widx), __ldg(Ws + widx), q, q2);
         }
       }
     }
 #pragma unroll
-    for (int r = 0; r < 16; r++) sm[smem_pad(base + r)] = v[r];
+    for (int r = 0; r < V; r++) sm[smem_pad(base + r)] = v[r];
     __syncthreads();
   }
+  const int32_t* __restrict__ oj = tab.own_j + h * B;
+  const int32_t* __restrict__ ok = tab.own_k + h * B;
 #pragma unroll
-  for (int r = 0; r < 16; r++) {
-    const int k = tid + r * T;
-    u64 x = sm[smem_pad(k)];
+  for (int r = 0; r < V; r++) {
+    const int idx = tid + r * T;
+    u64 x = sm[smem_pad(__ldg(ok + idx))];
     x = csub(x, q2);
     x = csub(x, q);
-    jb.store(k, x);
+    jb.store(__ldg(oj + idx), x);
   }
 }
 
 // ---------------------------------------------------------------------------------------
-// inverse transform; Job: bind(block) sets `limb`; load(k) returns a value in [0, 2q);
-// store(k, v) receives canonical v in [0, q).
+// inverse transform; Job: bind(poly) sets `limb`; load(j) (slot order) returns a value in
+// [0, 2q); store(k, v) receives canonical v in [0, q) for coefficient k.  Launched in clusters
+// of S CTAs.
 // ---------------------------------------------------------------------------------------
 template <int LOGN, class Job>
-__global__ void __launch_bounds__((1 << LOGN) / 16) ntt_inv_kernel(Job job, DevTables tab, LimbConsts L) {
-  constexpr int N = 1 << LOGN;
-  constexpr int T = N / 16;
-  constexpr int FULL = LOGN / 4;
-  constexpr int REM = LOGN % 4;
+__global__ void __launch_bounds__(NttCfg<LOGN>::T) ntt_inv_kernel(Job job, DevTables tab, LimbConsts L) {
+  using C = NttCfg<LOGN>;
+  constexpr int S = C::S, B = C::B, V = C::V, T = C::T;
   extern __shared__ u64 sm[];
   const int tid = threadIdx.x;
+  const int h = blockIdx.x % S;
   Job jb = job;
-  jb.bind(blockIdx.x);
+  jb.bind(blockIdx.x / S);
   const int l = jb.limb;
   const u64 q = L.lc[l].q, q2 = L.lc[l].two_q;
-  const u64* __restrict__ W = tab.ipsi_rev + (size_t)l * N;
-  const u64* __restrict__ Ws = tab.ipsi_rev_sh + (size_t)l * N;
-  u64 v[16];
+  const u64* __restrict__ W = tab.ipsi_rev + ((size_t)l << LOGN);
+  const u64* __restrict__ Ws = tab.ipsi_rev_sh + ((size_t)l << LOGN);
+  u64 v[V];
+  {
+    const int32_t* __restrict__ oj = tab.own_j + h * B;
+    const int32_t* __restrict__ ok = tab.own_k + h * B;
 #pragma unroll
-  for (int r = 0; r < 16; r++) {
-    const int k = tid + r * T;
-    sm[smem_pad(k)] = jb.load(k);
+    for (int r = 0; r < V; r++) {
+      const int idx = tid + r * T;
+      sm[smem_pad(__ldg(ok + idx))] = jb.load(__ldg(oj + idx));
+    }
   }
   __syncthreads();
 
+  // local stages: span t < B; global twiddle index (B / 2t)(S + h) + j / 2t
   int tlo = 1;
-  if constexpr (REM > 0) {
-    const int base = 16 * tid;
+  if constexpr (C::REM > 0) {
+    const int base = V * tid;
 #pragma unroll
-    for (int r = 0; r < 16; r++) v[r] = sm[smem_pad(base + r)];
+    for (int r = 0; r < V; r++) v[r] = sm[smem_pad(base + r)];
 #pragma unroll
-    for (int s = 0; s < REM; s++) {
+    for (int s = 0; s < C::REM; s++) {
       const int t = 1 << s;
-      const int h = N / (2 * t);
+      const int mloc = B / (2 * t);
 #pragma unroll
-      for (int r = 0; r < 16; r++) {
+      for (int r = 0; r < V; r++) {
         if ((r & t) == 0) {
           const int j = base + r;
-          const int widx = h + j / (2 * t);
+          const int widx = mloc * (S + h) + j / (2 * t);
           gs_bfly(v[r], v[r + t], __ldg(W + widx), __ldg(Ws + widx), q2);
         }
       }
     }
 #pragma unroll
-    for (int r = 0; r < 16; r++) sm[smem_pad(base + r)] = v[r];
+    for (int r = 0; r < V; r++) sm[smem_pad(base + r)] = v[r];
     __syncthreads();
-    tlo = 1 << REM;
+    tlo = 1 << C::REM;
   }
 #pragma unroll
-  for (int gi = 0; gi < FULL; gi++) {
-    const int delta = tlo;  // thi / 8 with thi = 8 tlo
-    const int base = (tid / delta) * (16 * delta) + (tid % delta);
+  for (int gi = 0; gi < C::FULL; gi++) {
+    const int delta = tlo;
+    const int base = (tid / delta) * (V * delta) + (tid % delta);
 #pragma unroll
-    for (int r = 0; r < 16; r++) v[r] = sm[smem_pad(base + r * delta)];
+    for (int r = 0; r < V; r++) v[r] = sm[smem_pad(base + r * delta)];
 #pragma unroll
-    for (int s = 0; s < 4; s++) {
+    for (int s = 0; s < C::LOGV; s++) {
       const int t = tlo << s;
       const int step = 1 << s;
-      const int h = N / (2 * t);
+      const int mloc = B / (2 * t);
 #pragma unroll
-      for (int r = 0; r < 16; r++) {
+      for (int r = 0; r < V; r++) {
         if ((r & step) == 0) {
           const int j = base + r * delta;
-          const int widx = h + j / (2 * t);
+          const int widx = mloc * (S + h) + j / (2 * t);
           gs_bfly(v[r], v[r + step], __ldg(W + widx), __ldg(Ws + widx), q2);
         }
       }
     }
-    if (gi + 1 < FULL) {
+    if (S > 1 || gi + 1 < C::FULL) {
 #pragma unroll
-      for (int r = 0; r < 16; r++) sm[smem_pad(base + r * delta)] = v[r];
+      for (int r = 0; r < V; r++) sm[smem_pad(base + r * delta)] = v[r];
       __syncthreads();
     } else {
-      // last group: delta = N/16, base = tid -> coefficient tid + r N/16; scale by N^{-1}
+      // last group of an unsplit transform: delta = B / V, base = tid -> coefficient tid + r T
       const u64 ni = L.lc[l].ninv, nis = L.lc[l].ninv_sh;
 #pragma unroll
-      for (int r = 0; r < 16; r++) {
+      for (int r = 0; r < V; r++) {
         u64 x = shoup_mul(v[r], ni, nis, q);
         jb.store(base + r * delta, csub(x, q));
       }
     }
-    tlo <<= 4;
+    tlo <<= C::LOGV;
+  }
+  if constexpr (S > 1) {
+    // cross-block stages (span t = span_b B): values of the S blocks at offset r through DSMEM
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    u64* peer[S];
+#pragma unroll
+    for (int g = 0; g < S; g++) peer[g] = cl.map_shared_rank(sm, g);
+    const u64 ni = L.lc[l].ninv, nis = L.lc[l].ninv_sh;
+#pragma unroll
+    for (int r = 0; r < V; r++) {
+      const int rr = tid + r * T;
+      u64 y[S];
+#pragma unroll
+      for (int g = 0; g < S; g++) y[g] = peer[g][smem_pad(rr)];
+#pragma unroll
+      for (int st = 0; st < C::LOGS; st++) {
+        const int span = 1 << st;
+#pragma unroll
+        for (int g = 0; g < S; g++)
+          if ((g & span) == 0) {
+            const int widx = S / (2 * span) + g / (2 * span);
+            gs_bfly(y[g], y[g + span], __ldg(W + widx), __ldg(Ws + widx), q2);
+          }
+      }
+      u64 x = y[0];
+#pragma unroll
+      for (int g = 1; g < S; g++)
+        if (g == h) x = y[g];
+      x = shoup_mul(x, ni, nis, q);
+      jb.store(h * B + rr, csub(x, q));
+    }
+    cl.sync();  // peers may still read this CTA's shared memory
   }
 }
 
 // ---------------------------------------------------------------------------------------
-// automorphism X -> X^g in the bit-reversed NTT domain:
-// out[k] = in[perm(k)], 2 bitrev(perm(k)) + 1 = (2 bitrev(k) + 1) g  (mod 2N)
+// automorphism X -> X^g on a slot-ordered NTT vector: out[j] = in[galois_perm(j)]
 // ---------------------------------------------------------------------------------------
-__device__ __forceinline__ int auto_perm(int k, uint32_t g, int logN) {
-  const uint32_t twoN_mask = (2u << logN) - 1u;
-  uint32_t e = ((__brev((uint32_t)k) >> (32 - logN)) * 2u + 1u) * g & twoN_mask;
-  return (int)(__brev((e - 1u) >> 1) >> (32 - logN));
+__device__ __forceinline__ int galois_perm(int j, GaloisAct a, int half) {
+  return ((j + (int)a.shift) & (half - 1)) | ((j & half) ^ (a.swap ? half : 0));
 }
 
 template <int LOGN>
 inline size_t ntt_smem_bytes() {
-  return (size_t)((1 << LOGN) + (1 << LOGN) / 16) * sizeof(u64);
+  constexpr int B = NttCfg<LOGN>::B;
+  return (size_t)(B + B / 16) * sizeof(u64);
 }

@@ -295,14 +295,17 @@ def _weight(Wt: np.ndarray, p: Plan, o: int, c: int, tau: int) -> int:
 
 
 def rotations(P: bfv.BFVParams, p: Plan, ct_in: np.ndarray, keys: Dict[int, np.ndarray],
-              units: Optional[List[int]] = None) -> Dict[Tuple[int, int], np.ndarray]:
-    """R[(ct, tau)]: every input ciphertext rotated by every tap step, hoisted
-    (PermDecomp once per ciphertext, PermAuto per tap)."""
+              units: Optional[List[int]] = None, cts: Optional[List[int]] = None
+              ) -> Dict[Tuple[int, int], np.ndarray]:
+    """R[(ct, tau)]: every input ciphertext (of `units`, or exactly the ciphertexts `cts`) rotated
+    by every tap step, hoisted (PermDecomp once per ciphertext, PermAuto per tap;
+    PAPER.md:375-377, 1590-1591)."""
     R = {}
     units = range(p.U) if units is None else units
-    for u in units:
-        for j in range(p.Jc):
-            ci = u * p.Jc + j
+    if cts is None:
+        cts = [u * p.Jc + j for u in units for j in range(p.Jc)]
+    for ci in cts:
+        if True:
             digits = bfv.decompose(P, ct_in[ci])
             for tau, (_, _, s) in enumerate(p.taps):
                 if s % (p.N // 2) == 0:
@@ -323,7 +326,10 @@ def he_conv(P: bfv.BFVParams, ls: LayerSetup, Wt: np.ndarray, ct_in: np.ndarray,
     out_cts = list(range(p.Jout)) if out_cts is None else list(out_cts)
     units = sorted({oc // p.Jo for oc in out_cts})
     if R is None:
-        R = rotations(P, p, ct_in, keys, units)
+        if p.depthwise:     # a depthwise output reads only its own channel's ciphertext
+            R = rotations(P, p, ct_in, keys, cts=sorted({oc // p.Jo * p.Jc + oc % p.Jo for oc in out_cts}))
+        else:
+            R = rotations(P, p, ct_in, keys, units)
     T = len(p.taps)
     res = {}
     S = sign_poly(P, ls) if p.cn == 2 else None

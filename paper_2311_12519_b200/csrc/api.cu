@@ -428,7 +428,11 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
     w->wblocks = 1;
   }
   w->Mpad = hy_mac_mpad(w->M);
-  w->Kpad = (w->K + 15) / 16 * 16;  // multiple of every K chunk (2 WM <= 16)
+  {
+    const int tile = hy_mac_tile(w->M);
+    const int kc = tile > 0 ? 2 * tile : 1;  // K chunk of the GEMM kernel (ksmac_gemm_kernel)
+    w->Kpad = (w->K + kc - 1) / kc * kc;
+  }
   // weight table (S0), [block][kk][row] as exact doubles; row semantics documented in DESIGN.md §4
   std::vector<double> wt((size_t)w->wblocks * w->Kpad * w->Mpad, 0.0);
   const uint32_t Ci = sh->Ci, Co = dw ? sh->Ci : sh->Co, kw = sh->kw;
@@ -494,6 +498,7 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
       {&w->d_C0, Jin * L * N},
       {&w->d_P, Jo * ctw * ((lay.cn == 2 && !dw) ? 2 : 1)},
       {&w->d_D2, (lay.cn == 2 && !dw) ? Jo * L * L * N + Jo * L * N : 0},
+      {&w->d_X, (lay.cn == 2 && !dw) ? Jo * ctw : 0},
       {&w->d_in, Jin * ctw},
       {&w->d_out, Jo * ctw},
   };
@@ -536,6 +541,7 @@ extern "C" void hy_weights_destroy(hy_weights* w) {
   cudaFree(w->d_C0);
   cudaFree(w->d_P);
   cudaFree(w->d_D2);
+  cudaFree(w->d_X);
   cudaFree(w->d_in);
   cudaFree(w->d_out);
   cudaFree(w->d_tap_keys);
@@ -666,7 +672,7 @@ extern "C" hy_status hy_rotate(hy_params* p, const uint64_t* ct_in, uint32_t g, 
   u64* work = nullptr;
   GaloisAct act;
   HY_CHECK(hy_galois_act(g, p->N, &act), HY_EINVAL, "Galois element %u is not odd / < 2N", g);
-  HY_CUDA_TRY(cudaMalloc(&work, n * (p->L * p->L + p->L) * p->N * sizeof(u64)));
+  HY_CUDA_TRY(cudaMalloc(&work, n * (p->L * p->L + 3 * p->L) * p->N * sizeof(u64)));
   hy_status st = hyk::rotate_ct(p, ct_in, act, it->second.ntt, ct_out, n, work, s);
   cudaError_t ce = cudaStreamSynchronize(s);
   cudaFree(work);

@@ -131,6 +131,7 @@ struct hy_weights {
   u64* d_C0;        // [U*Jc][L][N]    NTT(c0)
   u64* d_P;         // [U*Jo][cn'][2][L][N] partial sums (NTT form)
   u64* d_D2;        // [U*Jo][L][L][N] digits of P_{g,1}.c1 for the row swap
+  u64* d_X;         // [U*Jo][2][L][N] aligned outputs (NTT form) before the final INTT
   u64* d_in;        // staging for hy_conv_eval_host
   u64* d_out;
   u64** d_tap_keys;            // device array of key pointers per tap (nullptr = identity)

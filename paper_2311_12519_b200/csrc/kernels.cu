@@ -126,68 +126,67 @@ struct DigitLiftJob {
   __device__ void store(int k, u64 v) const { d[k] = v; }
 };
 
-// PermAuto value (S2): for limb l, NTT slot k,
-//   c0' = C0[perm(k)] + sum_i D_i[perm(k)] * b_{i,l}[k],  c1' = sum_i D_i[perm(k)] * a_{i,l}[k]
-// key layout [L digit][2][L limb][N] values, then the same block of Shoup companions.
-struct KSSrc {
-  const u64* c0;      // [L][N] NTT form for this ct (may be null: treated as 0)
-  const u64* D;       // [L digit][L limb][N]
-  const u64* diag;    // if non-null: digit i in limb i is diag[i*N + .] instead of D
-};
-
-__device__ __forceinline__ void ks_eval(const KSSrc& src, const u64* __restrict__ key, int L, int N, int l, int k, int kp,
-                                        const LimbConst& c, u64& o0, u64& o1) {
-  const u64 q = c.q, q2 = c.two_q;
-  const size_t kblk = (size_t)2 * L * L * N;
-  u64 a0 = src.c0 ? src.c0[(size_t)l * N + kp] : 0;
-  u64 a1 = 0;
-#pragma unroll 4
-  for (int i = 0; i < L; i++) {
-    const u64 dv = (src.diag && i == l) ? src.diag[(size_t)i * N + kp] : src.D[((size_t)i * L + l) * N + kp];
-    const size_t ib = ((size_t)(2 * i) * L + l) * N + k;
-    const size_t ia = ((size_t)(2 * i + 1) * L + l) * N + k;
-    a0 = csub(a0 + shoup_mul(dv, __ldg(key + ib), __ldg(key + kblk + ib), q), q2);
-    a1 = csub(a1 + shoup_mul(dv, __ldg(key + ia), __ldg(key + kblk + ia), q), q2);
-  }
-  o0 = a0;  // [0, 2q)
-  o1 = a1;
-}
-
-// Inverse transform whose input is a key-switched (rotated) ciphertext, optionally plus an
-// addend (the row-swap alignment Out = P_{g,0} + HRot(P_{g,1})), written to
-// coefficient form: hy_rotate and S4+S5.
-struct KSFinishJob {
-  // per output o: c0 source, D source (+ optional diag), addend (NTT form [2][L][N])
+// Key switching of whole ciphertexts (hy_rotate, S4 alignment), elementwise in the slot-order
+// NTT domain, one thread per (output, limb, position):
+//   X.c0[j] = c0[perm(j)] + sum_i D_i[perm(j)] b_i[j] (+ add.c0[j]),  X.c1[j] = sum_i D_i[perm(j)] a_i[j] (+ add.c1[j])
+// digit i in limb l is read from `diag` (the ct's own c1 limb, already NTT(d_l) in limb l) when
+// given.  The result is then brought back to coefficient form by a plain inverse transform.
+struct KsApplyArgs {
   const u64* c0;
   size_t c0_stride;
-  const u64* D;
+  const u64* D;  // [o][L digit][L limb][N]
   size_t D_stride;
   const u64* diag;
   size_t diag_stride;
-  const u64* add;
+  const u64* add;  // [o][2][L][N] or null
   size_t add_stride;
   const u64* key;
   GaloisAct act;
-  u64* out;  // [o][2][L][N]
-  int L, N, logN;
+  u64* out;  // [o][2][L][N] NTT form
+  int L, logN;
+  size_t total;  // nout * L * N
   LimbConsts lcs;
-  int limb, comp, o;
-  __device__ void bind(int b) {
-    o = b / (2 * L);
-    comp = (b / L) % 2;
-    limb = b % L;
-  }
-  __device__ u64 load(int k) const {
-    const int kp = galois_perm(k, act, N >> 1);
-    KSSrc src{c0 + (size_t)o * c0_stride, D + (size_t)o * D_stride, diag ? diag + (size_t)o * diag_stride : nullptr};
-    u64 r0, r1;
-    ks_eval(src, key, L, N, limb, k, kp, lcs.lc[limb], r0, r1);
-    u64 v = comp ? r1 : r0;
-    if (add) v = csub(v + add[(size_t)o * add_stride + ((size_t)comp * L + limb) * N + k], lcs.lc[limb].two_q);
-    return v;
-  }
-  __device__ void store(int k, u64 v) const { out[(((size_t)o * 2 + comp) * L + limb) * N + k] = v; }
 };
+
+__global__ void __launch_bounds__(256) ks_apply_kernel(KsApplyArgs a) {
+  const size_t idx = (size_t)blockIdx.x * 256 + threadIdx.x;
+  if (idx >= a.total) return;
+  const int N = 1 << a.logN, L = a.L;
+  const int j = (int)(idx & (N - 1));
+  const size_t ol = idx >> a.logN;
+  const int l = (int)(ol % L);
+  const size_t o = ol / L;
+  const LimbConst& c = a.lcs.lc[l];
+  const u64 q = c.q, q2 = c.two_q;
+  const int jp = galois_perm(j, a.act, N >> 1);
+  const size_t LN = (size_t)L * N, kblk = 2 * L * LN;
+  const u64* D = a.D + o * a.D_stride;
+  const u64* kb = a.key + (size_t)l * N + j;
+  u64 a0 = __ldg(a.c0 + o * a.c0_stride + (size_t)l * N + jp), a1 = 0;
+  for (int i = 0; i < L; i++) {
+    const u64 dv = (a.diag && i == l) ? __ldg(a.diag + o * a.diag_stride + (size_t)i * N + jp)
+                                      : __ldg(D + ((size_t)i * L + l) * N + jp);
+    const u64* k0 = kb + (size_t)(2 * i) * LN;
+    const u64* k1 = k0 + LN;
+    a0 = csub(a0 + shoup_mul(dv, __ldg(k0), __ldg(k0 + kblk), q), q2);
+    a1 = csub(a1 + shoup_mul(dv, __ldg(k1), __ldg(k1 + kblk), q), q2);
+  }
+  if (a.add) {
+    const u64* ad = a.add + o * a.add_stride + (size_t)l * N + j;
+    a0 = csub(a0 + __ldg(ad), q2);
+    a1 = csub(a1 + __ldg(ad + LN), q2);
+  }
+  u64* dst = a.out + o * 2 * LN + (size_t)l * N + j;
+  dst[0] = csub(a0, q);
+  dst[LN] = csub(a1, q);
+}
+
+hy_status launch_ks_apply(const KsApplyArgs& a, cudaStream_t s) {
+  if (!a.total) return HY_OK;
+  ks_apply_kernel<<<(unsigned)((a.total + 255) / 256), 256, 0, s>>>(a);
+  HY_LAUNCH_CHECK();
+  return HY_OK;
+}
 
 // plain INTT of an NTT-form ct array [o][cn'][2][L][N] picking diagonal 0 -> ct_out [o][2][L][N]
 struct OutInvJob {
@@ -774,23 +773,25 @@ hy_status finish_outputs(const hy_weights* w, size_t nunits, u64* ct_out, cudaSt
       DigitLiftJob jb{dig, w->d_D2, (int)L, (int)N, qarr(p)};
       HY_TRY(launch_fwd(p, jb, nout * L * (L - 1), s));
     }
-    KSFinishJob jc;
-    jc.c0 = w->d_P + ct_words;  // P_{g,1}.c0
-    jc.c0_stride = 2 * ct_words;
-    jc.D = w->d_D2;
-    jc.D_stride = L * L * N;
-    jc.diag = w->d_P + ct_words + L * N;  // P_{g,1}.c1: digit i in limb i is already NTT(d_i)
-    jc.diag_stride = 2 * ct_words;
-    jc.add = w->d_P;  // P_{g,0}
-    jc.add_stride = 2 * ct_words;
-    jc.key = w->d_swap_key;
-    jc.act = GaloisAct{0u, 1u};  // X -> X^{2N-1}: exchange the two slot rows
-    jc.out = ct_out;
-    jc.L = (int)L;
-    jc.N = (int)N;
-    jc.logN = (int)p->logN;
-    jc.lcs = limb_consts(p);
-    return launch_inv(p, jc, nout * 2 * L, s);
+    KsApplyArgs ka;
+    ka.c0 = w->d_P + ct_words;  // P_{g,1}.c0
+    ka.c0_stride = 2 * ct_words;
+    ka.D = w->d_D2;
+    ka.D_stride = L * L * N;
+    ka.diag = w->d_P + ct_words + L * N;  // P_{g,1}.c1: digit i in limb i is already NTT(d_i)
+    ka.diag_stride = 2 * ct_words;
+    ka.add = w->d_P;  // P_{g,0}
+    ka.add_stride = 2 * ct_words;
+    ka.key = w->d_swap_key;
+    ka.act = GaloisAct{0u, 1u};  // X -> X^{2N-1}: exchange the two slot rows
+    ka.out = w->d_X;
+    ka.L = (int)L;
+    ka.logN = (int)p->logN;
+    ka.total = nout * L * N;
+    ka.lcs = limb_consts(p);
+    HY_TRY(launch_ks_apply(ka, s));
+    OutInvJob jx{w->d_X, ct_words, ct_out, (int)L, (int)N};
+    return launch_inv(p, jx, nout * 2 * L, s);
   }
   OutInvJob j{w->d_P, ct_words, ct_out, (int)L, (int)N};
   return launch_inv(p, j, nout * 2 * L, s);
@@ -802,23 +803,26 @@ hy_status rotate_ct(const hy_params* p, const u64* ct_in, GaloisAct act, const u
   u64* D = work;
   u64* C0 = work + n * L * L * N;
   HY_TRY(permdecomp(p, ct_in, n, D, C0, s));
-  KSFinishJob j;
-  j.c0 = C0;
-  j.c0_stride = L * N;
-  j.D = D;
-  j.D_stride = L * L * N;
-  j.diag = nullptr;
-  j.diag_stride = 0;
-  j.add = nullptr;
-  j.add_stride = 0;
-  j.key = key;
-  j.act = act;
-  j.out = ct_out;
-  j.L = (int)L;
-  j.N = (int)N;
-  j.logN = (int)p->logN;
-  j.lcs = limb_consts(p);
-  return launch_inv(p, j, n * 2 * L, s);
+  u64* X = work + n * (L * L + L) * N;  // [n][2][L][N]
+  KsApplyArgs ka;
+  ka.c0 = C0;
+  ka.c0_stride = L * N;
+  ka.D = D;
+  ka.D_stride = L * L * N;
+  ka.diag = nullptr;
+  ka.diag_stride = 0;
+  ka.add = nullptr;
+  ka.add_stride = 0;
+  ka.key = key;
+  ka.act = act;
+  ka.out = X;
+  ka.L = (int)L;
+  ka.logN = (int)p->logN;
+  ka.total = n * L * N;
+  ka.lcs = limb_consts(p);
+  HY_TRY(launch_ks_apply(ka, s));
+  OutInvJob jx{X, 2 * L * N, ct_out, (int)L, (int)N};
+  return launch_inv(p, jx, n * 2 * L, s);
 }
 
 hy_status decrypt_phase(const hy_params* p, const u64* s_ntt, const u64* s_ntt_sh, const u64* ct, size_t n, u64* x_out,

@@ -3,11 +3,15 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
 
-A step = one hy_conv_eval of the configured layer (all of SURVEY §8(a): PermDecomp, PermAuto,
-lazy MAC + WHT + reduction + sign PMult, row-swap alignment, INTT) on synthetic ciphertexts
-already resident in HBM.  Default workload: BASELINE.json configs[1] (C2, ResNet-20-style layer,
-N = 8192, L = 3).  Multi-GPU (torchrun): every rank evaluates its own layer instance (weak scaling,
-no data-path collective); the time is the max over ranks.
+A step = one hy_conv_eval of the configured layer (all of SURVEY §8(a): PermDecomp, PermAuto fused
+with the lazy MAC + WHT + reduction + sign PMult, row-swap alignment, INTT) on synthetic
+ciphertexts already resident in HBM.  Default workload: BASELINE.json configs[1] (C2,
+ResNet-20-style layer, N = 8192, L = 3), the configuration the metric is quoted on.
+Multi-GPU (torchrun), --mode replica (default): every rank evaluates its own layer instance on
+its own images (weak scaling, no data-path collective); --mode shard: the ranks split ONE layer
+(units or output channels, paper_2311_12519_b200/shard.py) and rank 0 gathers the output
+ciphertexts with NCCL (strong scaling; the gather is inside the timed step).  The time is the
+max over ranks of CUDA-event time.
 
 Inputs are uniformly random ciphertexts and switching keys (synth/): under RLWE a real
 encryption is indistinguishable from uniform, and the kernels' work does not depend on the values.
@@ -42,24 +46,6 @@ def load_peaks():
         return json.load(open(PEAKS_PATH))
     except Exception:
         return {}
-
-
-# --------------------------------------------------------------------------------------------
-# workload accounting
-# --------------------------------------------------------------------------------------------
-def layer_work(cfg, lay):
-    """Method coefficient-MACs and algorithmic bytes of one layer."""
-    L, N, T = len(cfg.primes), cfg.N, lay.n_taps
-    ctw = 2 * L * N
-    if cfg.depthwise:
-        M, K, units = (2 if lay.cn == 2 else 1), T, lay.U * lay.Jc
-    else:
-        M, K, units = (4 * lay.Jo if lay.cn == 2 else lay.Jo), lay.Jc * T, lay.U
-    mac = M * K * ctw * units                       # coefficient MACs of S3 (2 DFMA each)
-    rot = lay.J * sum(1 for s in lay.tap_step[:T] if s % (N // 2))
-    swaps = lay.Jout if (lay.cn == 2 and not cfg.depthwise) else 0
-    return dict(coef_macs=mac, dfma=2 * mac, rotations=rot, rowswaps=swaps, ct_words=ctw,
-                in_bytes=lay.J * ctw * 8, out_bytes=lay.Jout * ctw * 8, M=M, K=K, units=units)
 
 
 class ClockSampler:
@@ -115,115 +101,172 @@ class ClockSampler:
 # --------------------------------------------------------------------------------------------
 # GPU arm
 # --------------------------------------------------------------------------------------------
+STAGES = ["S1_permdecomp", "S2S3_ksmac_wht", "S4S5_align_intt"]
+
+
 def run_gpu(args, cfg, rank, world):
     import torch
     import paper_2311_12519_b200 as hy
     from paper_2311_12519_b200 import build
+    from paper_2311_12519_b200 import shard as shard_mod
 
     if rank == 0 or not os.path.exists(hy.library_path()):
         build.build()
+    dist = None
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
     dev = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(dev)
-    lay0 = hy.hy_plan_layout(cfg.N, cfg.t, **cfg.shape_dict())
-    L = len(cfg.primes)
+    device = f"cuda:{dev}"
+    L, N = len(cfg.primes), cfg.N
+    full = hy.hy_plan_layout(cfg.N, cfg.t, **cfg.shape_dict())
+    W_full = synth.gen_weights(cfg)
+    shard = None
+    if args.mode == "shard" and world > 1:
+        shard = shard_mod.plan_shard(hy.layout_dict(full), cfg.shape_dict(), world, rank)
+        shape, W = shard.shape, shard_mod.slice_weights(W_full, shard)
+        ct_full = synth.gen_uniform_cts(cfg.primes, full.J, cfg.N, cfg.index, stream=0)
+        ct_host = np.ascontiguousarray(ct_full[shard.in_index])
+    else:                   # replica: this rank's own images through the whole layer
+        shape, W = cfg.shape_dict(), W_full
+        ct_host = synth.gen_uniform_cts(cfg.primes, full.J, cfg.N, cfg.index, stream=rank)
     p = hy.hy_params_create(cfg.N, cfg.primes, cfg.t, dev)
-    elts = list(lay0.galois[:lay0.n_galois])
-    keys = synth.gen_uniform_keys(cfg.primes, len(elts), cfg.N, cfg.index, stream=rank)
-    hy.hy_keys_upload(p, elts, keys)
-    W = synth.gen_weights(cfg)
-    w = hy.hy_encode_weights(p, W, **cfg.shape_dict())
-    lay = hy.hy_weights_layout(w)
-    work = layer_work(cfg, lay)
-    J, Jout = lay.J, lay.Jout
-    ct_host = synth.gen_uniform_cts(cfg.primes, J, cfg.N, cfg.index, stream=rank)
-    ct_in = torch.from_numpy(ct_host).to(f"cuda:{dev}")
-    ct_out = torch.empty((Jout, 2, L, cfg.N), dtype=torch.uint64, device=f"cuda:{dev}")
-    stream = torch.cuda.current_stream()
-    flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=f"cuda:{dev}")  # > 126 MB L2
+    elts = list(full.galois[:full.n_galois])
+    if elts:
+        hy.hy_keys_upload(p, elts, synth.gen_uniform_keys(cfg.primes, len(elts), cfg.N, cfg.index))
+    w = None
+    empty = shard is not None and shard.empty
+    if not empty:
+        w = hy.hy_encode_weights(p, W, **shape)
+        lay = hy.hy_weights_layout(w)
+        assert lay.J == len(ct_host)
+        ct_in = torch.from_numpy(ct_host).to(device)
+        ct_out = torch.empty((lay.Jout, 2, L, cfg.N), dtype=torch.uint64, device=device)
+    else:
+        lay = None
+        ct_out = torch.empty((0, 2, L, cfg.N), dtype=torch.uint64, device=device)
+    flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=device)  # > 126 MB L2
+
+    def step():
+        if not empty:
+            hy.hy_conv_eval(w, ct_in, ct_out)
+        if shard is not None:
+            shard_mod.gather_outputs(ct_out, shard, full.Jout)
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    hy.hy_weights_set_stage_events(w, ev)
+    if w is not None:
+        hy.hy_weights_set_stage_events(w, ev)
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(args.warmup):
-        hy.hy_conv_eval(w, ct_in, ct_out)
-    torch.cuda.synchronize()
-
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
+        step()
     torch.cuda.synchronize()
     step_ms, stage_ms = [], [[] for _ in range(3)]
     launches0 = hy.hy_kernel_launches()
     with ClockSampler(dev) as clk:
         for _ in range(args.steps):
             flush.zero_()                       # L2 flushed between timed iterations (untimed)
-            hy.hy_conv_eval(w, ct_in, ct_out)
-            ev[3].synchronize()
-            step_ms.append(ev[0].elapsed_time(ev[3]))
-            for i in range(3):
-                stage_ms[i].append(ev[i].elapsed_time(ev[i + 1]))
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0.record()
+            step()
+            t1.record()
+            t1.synchronize()
+            step_ms.append(t0.elapsed_time(t1))
+            if w is not None:
+                for i in range(3):
+                    stage_ms[i].append(ev[i].elapsed_time(ev[i + 1]))
     torch.cuda.synchronize()
     launches = hy.hy_kernel_launches() - launches0
     total_ms = sum(step_ms)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    if dist is not None:
+        t = torch.tensor([total_ms, float(launches)], dtype=torch.float64, device=device)
+        tl = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(tl, t)
+        total_ms = max(float(x[0].item()) for x in tl)          # max over ranks
+        launches = int(sum(float(x[1].item()) for x in tl))     # all ranks' kernels
         dist.barrier()
 
-    # end-to-end through the public host API: H2D of inputs and D2H of outputs inside the timing
-    hy.hy_weights_set_stage_events(w, [])
-    pin_in = torch.from_numpy(ct_host).pin_memory().numpy()
-    pin_out = torch.empty((Jout, 2, L, cfg.N), dtype=torch.uint64).pin_memory().numpy()
-    for _ in range(2):
-        hy.hy_conv_eval_host(w, pin_in, pin_out)
-    e2e_steps = max(3, min(args.steps, 50))
+    # end-to-end through the public host API: H2D of the inputs and D2H of the outputs inside
+    # the timed region, every step (hy_conv_eval_host synchronises its stream)
+    e2e_s, e2e_steps = None, max(3, min(args.steps, 50))
+    if w is not None:
+        hy.hy_weights_set_stage_events(w, [])
+        pin_in = torch.from_numpy(ct_host).pin_memory().numpy()
+        pin_out = torch.empty((lay.Jout, 2, L, cfg.N), dtype=torch.uint64).pin_memory().numpy()
+        for _ in range(2):
+            hy.hy_conv_eval_host(w, pin_in, pin_out)
     torch.cuda.synchronize()
-    if world > 1:
+    if dist is not None:
         dist.barrier()
-    t0 = time.perf_counter()
+    tt = time.perf_counter()
     for _ in range(e2e_steps):
-        hy.hy_conv_eval_host(w, pin_in, pin_out)   # synchronises the stream before returning
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{dev}")
+        if w is not None:
+            hy.hy_conv_eval_host(w, pin_in, pin_out)
+        if shard is not None:      # the gather runs on device buffers of the host call's outputs
+            shard_mod.gather_outputs(torch.from_numpy(pin_out).to(device) if w is not None else ct_out,
+                                     shard, full.Jout)
+    e2e_s = time.perf_counter() - tt
+    if dist is not None:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=device)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
 
-    hy.hy_weights_destroy(w)
+    if w is not None:
+        hy.hy_weights_destroy(w)
     hy.hy_params_destroy(p)
-    return dict(total_ms=total_ms, step_ms=step_ms, stage_ms=[statistics.mean(s) for s in stage_ms],
-                launches=launches, clocks=clk.summary(), work=work, lay=lay, e2e_s=e2e_s, e2e_steps=e2e_steps)
+    return dict(total_ms=total_ms, step_ms=step_ms,
+                stage_ms=[statistics.mean(s) if s else 0.0 for s in stage_ms],
+                launches=launches, clocks=clk.summary(), lay=lay, full=full, e2e_s=e2e_s, e2e_steps=e2e_steps,
+                in_bytes=len(ct_host) * 2 * L * N * 8, out_bytes=(lay.Jout if lay else 0) * 2 * L * N * 8)
+
+
+def layer_work(cfg, lay):
+    """Algorithmic work of one hy_conv_eval on layout `lay`:
+    coefficient-MACs of the fused S2+S3 kernel (M MAC rows x K terms x 2LN columns per unit;
+    c_n = 2 has 4 rows per output ct = 2 diagonals x 2 slot rows), 2 exact
+    DFMA each (30-bit halves); hoisted rotations; row swaps."""
+    L, N, T = len(cfg.primes), cfg.N, lay.n_taps
+    ctw = 2 * L * N
+    if cfg.depthwise:
+        M, K, units = (2 if lay.cn == 2 else 1), T, lay.U * lay.Jc
+    else:
+        M, K, units = (4 * lay.Jo if lay.cn == 2 else lay.Jo), lay.Jc * T, lay.U
+    mac = M * K * ctw * units
+    rot = lay.J * sum(1 for s in lay.tap_step[:T] if s % (N // 2))
+    swaps = lay.Jout if (lay.cn == 2 and not cfg.depthwise) else 0
+    return dict(coef_macs=mac, dfma=2 * mac, rotations=rot, rowswaps=swaps, M=M, K=K, units=units)
+
+
+def traffic_for(cfg_name, kernel):
+    """dram bytes per launch of `kernel` from the committed ncu capture (profiles/traffic.json)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))[cfg_name][kernel]
+    except Exception:
+        return None
 
 
 def roofline(cfg, res, peaks):
-    """Roofline of the dominant stage (largest mean time)."""
-    w = res["work"]
-    names = ["S1_permdecomp", "S2S3_ksmac_wht", "S4S5_align_intt"]
-    st = res["stage_ms"]
-    dom = int(np.argmax(st))
-    clk = res["clocks"]
-    clk_mhz = peaks.get("sm_max_mhz", 1965.0)
-    if dom == 1:
-        achieved = w["dfma"] / (st[1] * 1e-3) / 1e12
-        peak = DFMA_PER_CLK_SM * SM_COUNT * clk_mhz * 1e6 / 1e12
-        return {"kernel": names[dom], "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TDFMA/s",
-                "frac": achieved / peak, "traffic": None,
-                "peak_note": f"FP64 pipe {DFMA_PER_CLK_SM}/clk/SM x {SM_COUNT} SMs x sm_max {clk_mhz:.0f} MHz "
-                             "(derived; DESIGN.md)"}
-    L, N = len(cfg.primes), cfg.N
+    """Roofline of the fused S2+S3 kernel (ksmac: one launch per step, timed by the library's
+    stage events on its stream), the dominant kernel of every 3x3/1x1 dense config: bound by the
+    FP64 pipe that carries the exact MAC (2 DFMA per coefficient-MAC).  Peak = 64 DFMA/clk/SM x
+    148 SMs x the max SM clock (derived).  Depthwise layers are bound by the key
+    switching instead (int pipes / L2): reported against the same FP64 peak for comparability
+    plus their own stage split."""
     lay = res["lay"]
-    if dom == 0:
-        bytes_ = lay.J * (2 * L * N * 8 + (L * L + L) * N * 8)
-    else:
-        bytes_ = lay.Jout * (3 * 2 * L * N * 8)
-    hbm = peaks.get("hbm_gbs", 6547.2)
-    achieved = bytes_ / (st[dom] * 1e-3) / 1e9
-    return {"kernel": names[dom], "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": None}
+    w = layer_work(cfg, lay)
+    st = res["stage_ms"]
+    clk_mhz = res["clocks"].get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    achieved = w["dfma"] / (st[1] * 1e-3) / 1e12
+    peak = DFMA_PER_CLK_SM * SM_COUNT * clk_mhz * 1e6 / 1e12
+    dom = STAGES[int(np.argmax(st))]
+    return {"kernel": "ksmac_gemm_kernel (S2+S3)" if not cfg.depthwise else "ksmac_thin_kernel (S2+S3)",
+            "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TDFMA/s", "frac": achieved / peak,
+            "traffic": traffic_for(cfg.name, "ksmac"),
+            "kernel_ms": st[1], "share_of_step": st[1] / max(1e-9, sum(st)), "dominant_stage": dom,
+            "peak_note": f"FP64 pipe {DFMA_PER_CLK_SM}/clk/SM x {SM_COUNT} SMs x {clk_mhz:.0f} MHz (derived from "
+                         "the guide's unit counts; DESIGN.md §6)"}
 
 
 # --------------------------------------------------------------------------------------------
@@ -298,10 +341,11 @@ def run_reference(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="hyena", choices=["hyena", "reference"])
+    ap.add_argument("--mode", default="replica", choices=["replica", "shard"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"
@@ -315,33 +359,38 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{int(os.environ.get('LOCAL_RANK', 0))}"))
     res = run_gpu(args, cfg, rank, world)
     if rank == 0:
         peaks = load_peaks()
-        work, lay = res["work"], res["lay"]
+        full, lay = res["full"], res["lay"]
+        work = layer_work(cfg, full)
         ms = res["total_ms"] / args.steps
-        layers_s = world * args.steps / (res["total_ms"] * 1e-3)
-        gops = layers_s * work["coef_macs"] / 1e9
-        e2e = world * res["e2e_steps"] / res["e2e_s"]
+        shard = args.mode == "shard" and world > 1
+        layers_per_step = 1 if shard else world
+        layers_s = layers_per_step * args.steps / (res["total_ms"] * 1e-3)
+        e2e = layers_per_step * res["e2e_steps"] / res["e2e_s"]
         line = {
             "metric": METRIC, "value": layers_s, "unit": "layers/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u64 (exact modular int; MAC on the FP64 pipe, exact)",
-            "data": "synthetic (uniform ciphertexts + keys; RLWE-indistinguishable from real ones)",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if shard else "weak", "vs_baseline": None,
+            "dtype": "u64",
+            "data": "synthetic (uniform ciphertexts + keys: RLWE-indistinguishable from real encryptions; "
+                    "int8 weights uniform in the config's range)",
             "config": {"workload": f"{cfg.name}: Ci={cfg.Ci} Co={cfg.Co} H=W={cfg.H} {cfg.kh}x{cfg.kw} pad={cfg.pad} "
-                                   f"batch={cfg.batch} depthwise={cfg.depthwise}",
-                       "N": cfg.N, "L": len(cfg.primes), "t": cfg.t, "c_n": lay.cn, "k": lay.k, "J": lay.J,
-                       "Jout": lay.Jout, "rotations": work["rotations"], "rowswaps": work["rowswaps"],
-                       "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"replicas x{world}"},
-            "ct_mac_gops": gops,
-            "stages_ms": dict(zip(["S1_permdecomp", "S2S3_ksmac_wht", "S4S5_align_intt"],
-                                  res["stage_ms"])),
-            "roofline": roofline(cfg, res, peaks),
+                                   f"batch={cfg.batch} depthwise={cfg.depthwise} (BASELINE.json configs)",
+                       "N": cfg.N, "L": len(cfg.primes), "t": cfg.t, "c_n": full.cn, "k": full.k, "J": full.J,
+                       "Jout": full.Jout, "rotations": work["rotations"], "rowswaps": work["rowswaps"],
+                       "l2": "flushed between timed steps (256 MiB write, untimed)",
+                       "parallelism": (f"shard x{world} (units/output channels + NCCL gather to rank 0)" if shard
+                                       else f"replica x{world} (independent images per GPU)")},
+            "ct_mac_gops": layers_s * work["coef_macs"] / 1e9,
+            "stages_ms": dict(zip(STAGES, res["stage_ms"])),
+            "roofline": roofline(cfg, res, peaks) if lay is not None else None,
             "gpu_launches": res["launches"],
             "clocks": res["clocks"],
-            "e2e": {"value": e2e, "unit": "layers/s", "h2d_bytes_per_step": work["in_bytes"],
-                    "d2h_bytes_per_step": work["out_bytes"]},
+            "e2e": {"value": e2e, "unit": "layers/s", "h2d_bytes_per_step": res["in_bytes"],
+                    "d2h_bytes_per_step": res["out_bytes"]},
         }
         if world == 1 and not args.no_cpu_baseline:
             v, desc, _ = oracle_sample(cfg)

@@ -148,10 +148,11 @@ struct KsApplyArgs {
   LimbConsts lcs;
 };
 
+template <int LT>
 __global__ void __launch_bounds__(256) ks_apply_kernel(KsApplyArgs a) {
   const size_t idx = (size_t)blockIdx.x * 256 + threadIdx.x;
   if (idx >= a.total) return;
-  const int N = 1 << a.logN, L = a.L;
+  const int N = 1 << a.logN, L = LT > 0 ? LT : a.L;
   const int j = (int)(idx & (N - 1));
   const size_t ol = idx >> a.logN;
   const int l = (int)(ol % L);
@@ -163,7 +164,9 @@ __global__ void __launch_bounds__(256) ks_apply_kernel(KsApplyArgs a) {
   const u64* D = a.D + o * a.D_stride;
   const u64* kb = a.key + (size_t)l * N + j;
   u64 a0 = __ldg(a.c0 + o * a.c0_stride + (size_t)l * N + jp), a1 = 0;
-  for (int i = 0; i < L; i++) {
+#pragma unroll
+  for (int i = 0; i < (LT > 0 ? LT : HY_MAX_LIMBS); i++) {
+    if (LT == 0 && i >= L) break;
     const u64 dv = (a.diag && i == l) ? __ldg(a.diag + o * a.diag_stride + (size_t)i * N + jp)
                                       : __ldg(D + ((size_t)i * L + l) * N + jp);
     const u64* k0 = kb + (size_t)(2 * i) * LN;
@@ -183,7 +186,13 @@ __global__ void __launch_bounds__(256) ks_apply_kernel(KsApplyArgs a) {
 
 hy_status launch_ks_apply(const KsApplyArgs& a, cudaStream_t s) {
   if (!a.total) return HY_OK;
-  ks_apply_kernel<<<(unsigned)((a.total + 255) / 256), 256, 0, s>>>(a);
+  const unsigned blocks = (unsigned)((a.total + 255) / 256);
+  switch (a.L) {  // compile-time digit count: all loads of a thread issue at once
+    case 2: ks_apply_kernel<2><<<blocks, 256, 0, s>>>(a); break;
+    case 3: ks_apply_kernel<3><<<blocks, 256, 0, s>>>(a); break;
+    case 5: ks_apply_kernel<5><<<blocks, 256, 0, s>>>(a); break;
+    default: ks_apply_kernel<0><<<blocks, 256, 0, s>>>(a); break;
+  }
   HY_LAUNCH_CHECK();
   return HY_OK;
 }
@@ -393,7 +402,7 @@ template <int LT>
 struct KeyRegs {
   static constexpr int NL = LT > 0 ? LT : 1;
   u64 v[2 * NL], sh[2 * NL];
-  int tau = -1;
+  int tau = -1, pos = -1;
   __device__ __forceinline__ void load(const u64* __restrict__ key, int logN, int l, int j) {
     const size_t N = (size_t)1 << logN, LN = (size_t)LT * N, kblk = 2 * LT * LN;
     const u64* kb = key + (size_t)l * N + j;
@@ -465,9 +474,10 @@ __device__ __forceinline__ void r_value(const KsMacArgs& a, const u64* const* ke
   }
   const int jp = galois_perm(j, act[t], N >> 1);
   if constexpr (LT > 0) {
-    if (kr.tau != t) {
+    if (kr.tau != t || kr.pos != j) {
       kr.load(key, a.logN, l, j);
       kr.tau = t;
+      kr.pos = j;
     }
     ks_pair_regs<LT>(D, C0, kr, a.logN, l, jp, c, r0, r1);
   } else {

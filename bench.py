@@ -161,7 +161,7 @@ def run_gpu(args, cfg, rank, world):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    step_ms, stage_ms = [], [[] for _ in range(3)]
+    step_ms, stage_ms, mac_ms, mac_n = [], [[] for _ in range(3)], [], 0
     launches0 = hy.hy_kernel_launches()
     with ClockSampler(dev) as clk:
         for _ in range(args.steps):
@@ -177,6 +177,9 @@ def run_gpu(args, cfg, rank, world):
             if w is not None:
                 for i in range(3):
                     stage_ms[i].append(ev[i].elapsed_time(ev[i + 1]))
+                m, n = hy.hy_weights_mac_time(w)      # the MAC kernel's own launches
+                mac_ms.append(m)
+                mac_n += n
     torch.cuda.synchronize()
     launches = hy.hy_kernel_launches() - launches0
     total_ms = sum(step_ms)
@@ -218,6 +221,7 @@ def run_gpu(args, cfg, rank, world):
     hy.hy_params_destroy(p)
     return dict(total_ms=total_ms, step_ms=step_ms,
                 stage_ms=[statistics.mean(s) if s else 0.0 for s in stage_ms],
+                mac_ms=statistics.mean(mac_ms) if mac_ms else 0.0, mac_launches=mac_n,
                 launches=launches, clocks=clk.summary(), lay=lay, full=full, e2e_s=e2e_s, e2e_steps=e2e_steps,
                 in_bytes=len(ct_host) * 2 * L * N * 8, out_bytes=(lay.Jout if lay else 0) * 2 * L * N * 8)
 
@@ -247,24 +251,29 @@ def traffic_for(cfg_name, kernel):
         return None
 
 
-def roofline(cfg, res, peaks):
-    """Roofline of the fused S2+S3 kernel (ksmac: one launch per step, timed by the library's
-    stage events on its stream), the dominant kernel of every 3x3/1x1 dense config: bound by the
-    FP64 pipe that carries the exact MAC (2 DFMA per coefficient-MAC).  Peak = 64 DFMA/clk/SM x
-    148 SMs x the max SM clock (derived).  Depthwise layers are bound by the key
-    switching instead (int pipes / L2): reported against the same FP64 peak for comparability
-    plus their own stage split."""
+def roofline(cfg, res, peaks, steps):
+    """Roofline of the MAC kernel (S3: the exact lazy MAC + WHT + reduction + sign PMult; the
+    dominant kernel of every dense config), timed per launch by library-owned CUDA events on its
+    stream: bound by the FP64 pipe that carries the MAC (2 DFMA per coefficient-MAC).  Peak =
+    64 DFMA/clk/SM x 148 SMs x the max SM clock (derived).  Depthwise layers fuse
+    the key switching into a thin MAC and are bound by it (int pipes / L2): reported against the
+    same FP64 peak for comparability."""
     lay = res["lay"]
     w = layer_work(cfg, lay)
     st = res["stage_ms"]
     clk_mhz = res["clocks"].get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
-    achieved = w["dfma"] / (st[1] * 1e-3) / 1e12
+    kms = res["mac_ms"] or st[1]
+    achieved = w["dfma"] / (kms * 1e-3) / 1e12
     peak = DFMA_PER_CLK_SM * SM_COUNT * clk_mhz * 1e6 / 1e12
     dom = STAGES[int(np.argmax(st))]
-    return {"kernel": "ksmac_gemm_kernel (S2+S3)" if not cfg.depthwise else "ksmac_thin_kernel (S2+S3)",
+    per_step = max(1, res["mac_launches"] // max(1, steps))
+    name = ("ksmac_thin_kernel (fused S2+S3)" if cfg.depthwise else
+            "mac_gemm_kernel (S3)" if per_step > 0 and kms < st[1] * 0.999 else "ksmac_gemm_kernel (fused S2+S3)")
+    return {"kernel": name,
             "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TDFMA/s", "frac": achieved / peak,
-            "traffic": traffic_for(cfg.name, "ksmac"),
-            "kernel_ms": st[1], "share_of_step": st[1] / max(1e-9, sum(st)), "dominant_stage": dom,
+            "traffic": traffic_for(cfg.name, "mac"),
+            "kernel_ms_per_step": kms, "launches_per_step": per_step, "share_of_step": kms / max(1e-9, sum(st)),
+            "dominant_stage": dom,
             "peak_note": f"FP64 pipe {DFMA_PER_CLK_SM}/clk/SM x {SM_COUNT} SMs x {clk_mhz:.0f} MHz (derived from "
                          "the guide's unit counts; DESIGN.md §6)"}
 
@@ -386,7 +395,7 @@ def main():
                                        else f"replica x{world} (independent images per GPU)")},
             "ct_mac_gops": layers_s * work["coef_macs"] / 1e9,
             "stages_ms": dict(zip(STAGES, res["stage_ms"])),
-            "roofline": roofline(cfg, res, peaks) if lay is not None else None,
+            "roofline": roofline(cfg, res, peaks, args.steps) if lay is not None else None,
             "gpu_launches": res["launches"],
             "clocks": res["clocks"],
             "e2e": {"value": e2e, "unit": "layers/s", "h2d_bytes_per_step": res["in_bytes"],

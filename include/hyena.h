@@ -153,6 +153,11 @@ hy_status hy_rotate(hy_params* p, const uint64_t* ct_in, uint32_t galois_elt, ui
  * after S4+S5].  n = 0 clears them.  Errors: HY_EINVAL. */
 uint64_t hy_kernel_launches(void);
 hy_status hy_weights_set_stage_events(hy_weights* w, void* const* events, uint32_t n);
+/* While stage events are set, hy_conv_eval also brackets every launch of its MAC kernel (the
+ * fused S2+S3 kernel, or each batch of the MAC GEMM) with library-owned events; this returns the
+ * summed device time of those launches in the last evaluation and their count (synchronises on
+ * the last one).  Errors: HY_EINVAL, HY_ECUDA. */
+hy_status hy_weights_mac_time(const hy_weights* w, float* total_ms, uint32_t* launches);
 
 /* Debug decryption (PAPER.md:256-267 [\ignore]): for each of n device ciphertexts
  * [n][2][L][N] computes [c0 + c1 s]_{q_l} on the GPU, then on the host the exact CRT

@@ -296,6 +296,9 @@ extern "C" hy_status hy_params_create(uint32_t N, const uint64_t* q, uint32_t L,
     c.c30 = (1ull << 30) % ql;
     c.c30_sh = shoup(c.c30, ql);
     c.off = ql * (((1ull << 59) + ql - 1) / ql);
+    c.c32 = (1ull << 32) % ql;
+    c.c32_sh = shoup(c.c32, ql);
+    c.off62 = ql * (((1ull << 62) + ql - 1) / ql);
   }
   // slot-order position j <-> bit-reversed butterfly position k, split into the
   // NTT blocks of HY_NTT_BLOCK coefficients
@@ -428,11 +431,7 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
     w->wblocks = 1;
   }
   w->Mpad = hy_mac_mpad(w->M);
-  {
-    const int tile = hy_mac_tile(w->M);
-    const int kc = tile > 0 ? 2 * tile : 1;  // K chunk of the GEMM kernel (ksmac_gemm_kernel)
-    w->Kpad = (w->K + kc - 1) / kc * kc;
-  }
+  w->Kpad = (w->K + 31) / 32 * 32;  // multiple of the MAC K chunks (16 FP64 GEMM, 32 tcgen05)
   // weight table (S0), [block][kk][row] as exact doubles; row semantics documented in DESIGN.md §4
   std::vector<double> wt((size_t)w->wblocks * w->Kpad * w->Mpad, 0.0);
   const uint32_t Ci = sh->Ci, Co = dw ? sh->Ci : sh->Co, kw = sh->kw;
@@ -459,6 +458,21 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
         wt[((size_t)b * w->Kpad + kk) * w->Mpad + row] = (double)v;
       }
   hy_status st = upload((void**)&w->d_wt, wt.data(), wt.size() * sizeof(double));
+  if (st == HY_OK) {
+    // the same weights as int8 in the tcgen05 canonical K-major layout, 128-row x 32-term tiles:
+    // byte (row r, term k) of a tile at (r/8)*256 + (k/16)*128 + (r%8)*16 + k%16
+    const int mt = (w->Mpad + 127) / 128, kt = w->Kpad / 32;
+    std::vector<int8_t> w8((size_t)w->wblocks * mt * kt * 4096, 0);
+    for (int b = 0; b < w->wblocks; b++)
+      for (int row = 0; row < w->M; row++)
+        for (int kk = 0; kk < w->K; kk++) {
+          const int r = row % 128, k = kk % 32;
+          const size_t tile = ((size_t)b * mt + row / 128) * kt + kk / 32;
+          w8[tile * 4096 + (r / 8) * 256 + (k / 16) * 128 + (r % 8) * 16 + k % 16] =
+              (int8_t)wt[((size_t)b * w->Kpad + kk) * w->Mpad + row];
+        }
+    st = upload((void**)&w->d_w8, w8.data(), w8.size());
+  }
   if (st != HY_OK) {
     hy_weights_destroy(w);
     return st;
@@ -489,7 +503,14 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
       return st;
     }
   }
-  // workspace
+  // workspace; the rotated inputs R of the dense path are materialised for r_units units at a
+  // time (at most HY_R_BUDGET bytes)
+  {
+    const size_t per_unit = (size_t)w->K * ctw * sizeof(u64);
+    size_t ru = per_unit ? HY_R_BUDGET / per_unit : 1;
+    if (ru < 1) ru = 1;
+    w->r_units = (int)std::min<size_t>(ru, lay.U);
+  }
   struct A {
     u64** ptr;
     size_t words;
@@ -499,6 +520,7 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
       {&w->d_P, Jo * ctw * ((lay.cn == 2 && !dw) ? 2 : 1)},
       {&w->d_D2, (lay.cn == 2 && !dw) ? Jo * L * L * N + Jo * L * N : 0},
       {&w->d_X, (lay.cn == 2 && !dw) ? Jo * ctw : 0},
+      {&w->d_R, !dw ? (size_t)w->r_units * w->K * ctw : 0},
       {&w->d_in, Jin * ctw},
       {&w->d_out, Jo * ctw},
   };
@@ -526,6 +548,21 @@ extern "C" hy_status hy_weights_set_stage_events(hy_weights* w, void* const* eve
   return HY_OK;
 }
 
+extern "C" hy_status hy_weights_mac_time(const hy_weights* w, float* total_ms, uint32_t* launches) {
+  HY_CHECK(w && total_ms && launches, HY_EINVAL, "null argument");
+  *total_ms = 0.f;
+  *launches = 0;
+  if (!w->mac_ev || !w->mac_launches) return HY_OK;
+  for (uint32_t i = 0; i < w->mac_launches; i++) {
+    float ms = 0.f;
+    HY_CUDA_TRY(cudaEventSynchronize((*w->mac_ev)[2 * i + 1]));
+    HY_CUDA_TRY(cudaEventElapsedTime(&ms, (*w->mac_ev)[2 * i], (*w->mac_ev)[2 * i + 1]));
+    *total_ms += ms;
+  }
+  *launches = w->mac_launches;
+  return HY_OK;
+}
+
 extern "C" hy_status hy_weights_layout(const hy_weights* w, hy_layout* out) {
   HY_CHECK(w && out, HY_EINVAL, "null argument");
   *out = w->lay;
@@ -536,16 +573,22 @@ extern "C" void hy_weights_destroy(hy_weights* w) {
   if (!w) return;
   cudaSetDevice(w->p->device);
   cudaFree(w->d_wt);
+  cudaFree(w->d_w8);
   cudaFree(w->d_sign);
   cudaFree(w->d_D);
   cudaFree(w->d_C0);
   cudaFree(w->d_P);
   cudaFree(w->d_D2);
   cudaFree(w->d_X);
+  cudaFree(w->d_R);
   cudaFree(w->d_in);
   cudaFree(w->d_out);
   cudaFree(w->d_tap_keys);
   cudaFree(w->d_tap_act);
+  if (w->mac_ev) {
+    for (cudaEvent_t e : *w->mac_ev) cudaEventDestroy(e);
+    delete w->mac_ev;
+  }
   delete w;
 }
 

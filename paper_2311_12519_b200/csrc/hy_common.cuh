@@ -55,6 +55,8 @@ struct LimbConst {
   u64 one_sh;             // floor(2^64 / q): Shoup companion of 1
   u64 c30, c30_sh;        // 2^30 mod q and Shoup companion
   u64 off;                // q * ceil(2^59 / q): makes |x| < 2^59 signed values nonnegative
+  u64 c32, c32_sh;        // 2^32 mod q and Shoup companion (tensor-core MAC epilogue)
+  u64 off62;              // q * ceil(2^62 / q): makes |x| < 2^62 signed values nonnegative
 };
 
 struct DevTables {
@@ -78,7 +80,8 @@ struct GaloisAct {
   uint32_t swap;
 };
 
-#define HY_NTT_BLOCK 4096  // coefficients per NTT CTA (must match NttCfg in ntt.cuh)
+#define HY_NTT_BLOCK 4096
+#define HY_R_BUDGET ((size_t)4 << 30)  // bytes of materialised rotated inputs per hy_weights  // coefficients per NTT CTA (must match NttCfg in ntt.cuh)
 
 struct KeyEntry {
   uint32_t g;
@@ -125,6 +128,8 @@ struct hy_weights {
   int wblocks;      // number of distinct weight blocks (1 dense, Jc depthwise)
   int Mpad, Kpad;   // M rounded up to the row tile, K rounded up to the MAC chunk
   double* d_wt;     // [wblocks][Kpad][Mpad] weights (exact small integers), zero padded
+  int8_t* d_w8;     // [wblocks][Mpad/128][Kpad/32][4096]: weights as int8 in the tcgen05 K-major
+                    // no-swizzle canonical layout (tensor-core MAC), zero padded
   u64* d_sign;      // [L][N] NTT form of the [k,-k] plaintext, then [L][N] Shoup companions
   // workspace (device)
   u64* d_D;         // [U*Jc][L digit][L limb][N] NTT-form digits
@@ -132,6 +137,8 @@ struct hy_weights {
   u64* d_P;         // [U*Jo][cn'][2][L][N] partial sums (NTT form)
   u64* d_D2;        // [U*Jo][L][L][N] digits of P_{g,1}.c1 for the row swap
   u64* d_X;         // [U*Jo][2][L][N] aligned outputs (NTT form) before the final INTT
+  u64* d_R;         // [r_units][K][2][L][N] rotated inputs of the dense path (slot-order NTT)
+  int r_units;      // units per PermAuto + MAC batch
   u64* d_in;        // staging for hy_conv_eval_host
   u64* d_out;
   u64** d_tap_keys;            // device array of key pointers per tap (nullptr = identity)
@@ -140,6 +147,10 @@ struct hy_weights {
   u64 keys_version;            // params->keys_version the tap table was built from
   cudaEvent_t ev[4];           // optional stage-boundary events (bench)
   uint32_t n_ev;
+  // per-launch timing of the MAC kernel (enabled with the stage events): event pairs around each
+  // MAC launch of the last hy_conv_eval
+  std::vector<cudaEvent_t>* mac_ev;
+  uint32_t mac_launches;
 };
 
 // ------------------------------------------------------------------------------------
@@ -183,7 +194,7 @@ hy_status pointwise_mul(const hy_params* p, const u64* a, const u64* b, u64* c, 
 hy_status shoup_table(const hy_params* p, const u64* w, u64* w_sh, size_t npoly, cudaStream_t s);  // [n][L][N]
 hy_status key_to_ntt(const hy_params* p, const u64* key_coeff, u64* key_ntt, cudaStream_t s);
 hy_status permdecomp(const hy_params* p, const u64* ct, size_t nct, u64* D, u64* C0, cudaStream_t s);
-hy_status ksmac(const hy_weights* w, size_t nunits, cudaStream_t s);  // fused S2 + S3
+hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s);  // S2 + S3
 hy_status finish_outputs(const hy_weights* w, size_t nunits, u64* ct_out, cudaStream_t s);
 hy_status rotate_ct(const hy_params* p, const u64* ct_in, GaloisAct act, const u64* key, u64* ct_out, size_t n,
                     u64* work, cudaStream_t s);

@@ -1,5 +1,8 @@
 // Device kernels of the Hyena hot path and their launchers.
 #include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 #include "hy_common.cuh"
 #include "ntt.cuh"
@@ -654,6 +657,449 @@ __global__ void __launch_bounds__(256) ksmac_thin_kernel(KsMacArgs a) {
   for (int c = 0; c < 2; c++) store_outputs(a, z, 0, c, l, j, ah[c], al[c], MR);
 }
 
+// ------------------------------------------------------------------------------------------
+// Split variant of S2 + S3 for dense layers (the default): PermAuto materialises the rotated
+// inputs R[unit][kk][2][L][N] (kk = tau * Jc + c, slot-order NTT form), then a pure MAC GEMM
+// consumes them.  Keeping the key switching (INT pipes) out of the MAC kernel leaves the FP64
+// pipe's issue slots to the DFMAs (fused 42 %, split MAC ~70 % of the FP64 peak).
+// ------------------------------------------------------------------------------------------
+// PermAuto: one thread per (limb, position) of one tap and unit; the tap's key words for the
+// position stay in registers while the thread walks the unit's input ciphertexts.
+template <int LT>
+__global__ void __launch_bounds__(256) permauto_kernel(KsMacArgs a, u64* __restrict__ R) {
+  const int N = 1 << a.logN, L = LT > 0 ? LT : a.L;
+  const int idx = blockIdx.x * 256 + threadIdx.x;
+  const int l = idx >> a.logN, j = idx & (N - 1);
+  if (l >= L) return;
+  const int t = blockIdx.y, z = blockIdx.z;
+  const LimbConst cst = a.lcs.lc[l];
+  const size_t LN = (size_t)L * N;
+  const u64* key = a.keys[t];
+  u64* out = R + ((size_t)z * a.K + (size_t)t * a.Jcb) * 2 * LN + (size_t)l * N + j;
+  const u64* C0b = a.C0 + (size_t)z * a.Jcb * LN;
+  const u64* Db = a.D + (size_t)z * a.Jcb * L * LN;
+  if (key == nullptr) {  // identity tap: R = (C0, D_{l,l})
+    for (int c = 0; c < a.Jcb; c++) {
+      const u64 r0 = __ldg(C0b + (size_t)c * LN + (size_t)l * N + j);
+      const u64 r1 = __ldg(Db + (size_t)c * L * LN + ((size_t)l * L + l) * N + j);
+      __stcs(out + (size_t)c * 2 * LN, r0);
+      __stcs(out + (size_t)c * 2 * LN + LN, r1);
+    }
+    return;
+  }
+  const int jp = galois_perm(j, a.act[t], N >> 1);
+  if constexpr (LT > 0) {
+    KeyRegs<LT> kr;
+    kr.load(key, a.logN, l, j);
+    const u64* C0p = C0b + (size_t)l * N + jp;
+    const u64* Dp = Db + (size_t)l * N + jp;
+    // software pipeline: the reads of ciphertext c + 1 are in flight while c is key-switched
+    u64 c0n = __ldg(C0p), dn[LT];
+#pragma unroll
+    for (int i = 0; i < LT; i++) dn[i] = __ldg(Dp + (size_t)i * LN);
+    for (int c = 0; c < a.Jcb; c++) {
+      const u64 c0 = c0n;
+      u64 d[LT];
+#pragma unroll
+      for (int i = 0; i < LT; i++) d[i] = dn[i];
+      if (c + 1 < a.Jcb) {
+        c0n = __ldg(C0p + (size_t)(c + 1) * LN);
+#pragma unroll
+        for (int i = 0; i < LT; i++) dn[i] = __ldg(Dp + (size_t)(c + 1) * L * LN + (size_t)i * LN);
+      }
+      const u64 q = cst.q, q2 = cst.two_q;
+      u64 a0 = c0, a1 = 0;
+#pragma unroll
+      for (int i = 0; i < LT; i++) {
+        a0 = csub(a0 + shoup_mul(d[i], kr.v[2 * i], kr.sh[2 * i], q), q2);
+        a1 = csub(a1 + shoup_mul(d[i], kr.v[2 * i + 1], kr.sh[2 * i + 1], q), q2);
+      }
+      __stcs(out + (size_t)c * 2 * LN, csub(a0, q));
+      __stcs(out + (size_t)c * 2 * LN + LN, csub(a1, q));
+    }
+  } else {
+    for (int c = 0; c < a.Jcb; c++) {
+      u64 r0, r1;
+      ks_pair_any(Db + (size_t)c * L * LN, C0b + (size_t)c * LN, key, L, a.logN, l, j, jp, cst, r0, r1);
+      __stcs(out + (size_t)c * 2 * LN, r0);
+      __stcs(out + (size_t)c * 2 * LN + LN, r1);
+    }
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND) : "memory");
+}
+
+// MAC GEMM: C[M][2 x BNP] = W[M][K] x R[K][2 x BNP].  256 threads = WM row-group warps x PG
+// position groups; lane owns positions (pg*64 + lane, pg*64 + lane + 32) of both components
+// (8 rows x 4 columns of exact FP64 accumulators).  R (u64) and W chunks of KC = 16 terms stream
+// in through a 3-stage cp.async ring; each chunk is split once into (hi, lo) doubles in shared
+// memory and consumed by every row-group warp.
+constexpr int MG_STAGES = 3;
+
+template <int WM>
+struct MgTile {
+  static constexpr int BM = 8 * WM, PG = 8 / WM, BNP = 64 * PG, KC = WM >= 8 ? 16 : 8;
+  static constexpr size_t RAW = sizeof(u64) * KC * 2 * BNP;        // per stage
+  static constexpr size_t WSZ = sizeof(double) * KC * BM;           // per stage
+  static constexpr size_t RD = sizeof(double2) * KC * 2 * BNP;      // converted chunk
+  static constexpr size_t SMEM = MG_STAGES * (RAW + WSZ) + 2 * RD;  // Rd double-buffered
+};
+
+template <int WM>
+__global__ void __launch_bounds__(256, 1) mac_gemm_kernel(KsMacArgs a, const u64* __restrict__ R) {
+  using TL = MgTile<WM>;
+  constexpr int BM = TL::BM, BNP = TL::BNP, KC = TL::KC;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  auto raw = [&](int st) { return reinterpret_cast<u64*>(smraw + st * (TL::RAW + TL::WSZ)); };  // [KC][2][BNP]
+  auto wsm = [&](int st) { return reinterpret_cast<double*>(smraw + st * (TL::RAW + TL::WSZ) + TL::RAW); };
+  double2* Rd = reinterpret_cast<double2*>(smraw + MG_STAGES * (TL::RAW + TL::WSZ));  // [KC][2][BNP]
+
+  const int N = 1 << a.logN;
+  const size_t LN = (size_t)a.L * N;
+  const int tiles = N / BNP;
+  const int l = blockIdx.x / tiles, j0 = (blockIdx.x % tiles) * BNP;
+  const int row0 = blockIdx.y * BM, z = blockIdx.z;
+  const double* __restrict__ wt = a.wt + (size_t)(z % a.wblocks) * a.Kpad * a.Mpad;
+  const u64* __restrict__ Rz = R + (size_t)z * a.K * 2 * LN + (size_t)l * N + j0;
+  const int nchunks = a.Kpad / KC;
+
+  auto issue = [&](int ch) {
+    if (ch < nchunks) {
+      const int st = ch % MG_STAGES;
+      u64* dst = raw(st);
+      // R rows (kk, comp): BNP contiguous u64 = BNP/2 16-byte pieces
+      for (int e = threadIdx.x; e < KC * 2 * (BNP / 2); e += 256) {
+        const int row = e / (BNP / 2), piece = e % (BNP / 2);
+        const int kk = ch * KC + row / 2, comp = row % 2;
+        u64* d = dst + (size_t)row * BNP + piece * 2;
+        if (kk < a.K)
+          cp_async16(d, Rz + ((size_t)kk * 2 + comp) * LN + piece * 2);
+        else
+          d[0] = d[1] = 0;
+      }
+      double* wd = wsm(st);
+      for (int e = threadIdx.x; e < KC * BM / 2; e += 256) {
+        const int kk = e / (BM / 2), r2 = e % (BM / 2);
+        cp_async16(wd + kk * BM + 2 * r2, wt + (size_t)(ch * KC + kk) * a.Mpad + row0 + 2 * r2);
+      }
+    }
+    cp_async_commit();
+  };
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rg = warp % WM, pg = warp / WM;
+  const int p0 = pg * 64 + lane;
+  double acc_h[8][4], acc_l[8][4];
+#pragma unroll
+  for (int r = 0; r < 8; r++)
+#pragma unroll
+    for (int n = 0; n < 4; n++) acc_h[r][n] = acc_l[r][n] = 0.0;
+
+  auto convert = [&](int ch) {  // raw u64 chunk -> (hi, lo) doubles, split once for all warps
+    const u64* src = raw(ch % MG_STAGES);
+    double2* dst = Rd + (size_t)(ch & 1) * KC * 2 * BNP;
+    for (int e = threadIdx.x; e < KC * 2 * BNP; e += 256) {
+      const u64 x = src[e];
+      dst[e] = make_double2((double)(uint32_t)(x >> 30), (double)(uint32_t)(x & M30));
+    }
+  };
+#pragma unroll
+  for (int st = 0; st < MG_STAGES - 1; st++) issue(st);
+  cp_async_wait<MG_STAGES - 2>();
+  __syncthreads();
+  convert(0);
+  __syncthreads();
+  for (int ch = 0; ch < nchunks; ch++) {
+    issue(ch + MG_STAGES - 1);
+    const double* wd = wsm(ch % MG_STAGES);
+    const double2* Rc = Rd + (size_t)(ch & 1) * KC * 2 * BNP;
+#pragma unroll 4
+    for (int kk = 0; kk < KC; kk++) {
+      const double2* wp = reinterpret_cast<const double2*>(wd + kk * BM + rg * 8);
+      double w[8];
+#pragma unroll
+      for (int r = 0; r < 4; r++) {
+        const double2 t2 = wp[r];
+        w[2 * r] = t2.x;
+        w[2 * r + 1] = t2.y;
+      }
+      const double2* rp = Rc + (size_t)kk * 2 * BNP + p0;
+      double2 x[4];
+      x[0] = rp[0];
+      x[1] = rp[32];
+      x[2] = rp[BNP];
+      x[3] = rp[BNP + 32];
+#pragma unroll
+      for (int r = 0; r < 8; r++)
+#pragma unroll
+        for (int n = 0; n < 4; n++) {
+          acc_h[r][n] = fma(w[r], x[n].x, acc_h[r][n]);
+          acc_l[r][n] = fma(w[r], x[n].y, acc_l[r][n]);
+        }
+    }
+    if (ch + 1 < nchunks) {
+      cp_async_wait<MG_STAGES - 2>();  // chunk ch + 1 landed (this thread's copies)
+      __syncthreads();                 // ... everyone's; stage ch % S and Rd[(ch+1)&1] are free
+      convert(ch + 1);
+      __syncthreads();
+    }
+  }
+  cp_async_wait<0>();
+#pragma unroll
+  for (int n = 0; n < 4; n++) {
+    double ah[8], al[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      ah[r] = acc_h[r][n];
+      al[r] = acc_l[r][n];
+    }
+    store_outputs(a, z, row0 + rg * 8, n >> 1, l, j0 + p0 + 32 * (n & 1), ah, al, 8);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Tensor-core MAC (tcgen05, kind::i8).  The lazy MAC is an exact integer contraction
+// B[m][col] = sum_kk w[m][kk] R[kk][col] with |w| <= 128 and R < 2^60: split every R value into
+// its 8 bytes, R = sum_b 2^{8b} R_b, and B = sum_b 2^{8b} (W x R_b) with one s8 x u8 -> s32 MMA per
+// byte plane.  |W x R_b| <= 128 * 255 * K < 2^31 for K <= 2^16 (the planner's bound), so every
+// accumulator is exact; the epilogue recombines the planes as two int64 halves
+// S = S_hi 2^32 + S_lo and reduces once per output coefficient.
+// CTA = one unit, one limb, 16 positions x 2 components (32 columns), 128 MAC rows; 4 producer
+// warps stream R chunks of 32 terms from HBM and transpose them into the 8 byte planes (K-major
+// canonical smem layout), one thread issues 8 UMMAs (M=128, N=32, K=32) per chunk into 8 TMEM
+// accumulators (256 columns), and the producer warps run the epilogue from TMEM.
+// ------------------------------------------------------------------------------------------
+constexpr int TC_STAGES = 3, TC_COLS = 32, TC_POS = 16, TC_THREADS = 160;
+constexpr uint32_t TC_TMEM_COLS = 8 * TC_COLS;  // 256
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr) {
+  // K-major, no swizzle: core matrices of 8 rows x 16 bytes; LBO (next 16 bytes of K) = 128 B,
+  // SBO (next 8 rows) = 256 B; version 1 (sm_100)
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(128 >> 4) << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+
+__device__ __forceinline__ uint32_t umma_idesc_s8u8(int m, int n) {
+  return (2u << 4) | (1u << 7) | (0u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  }
+}
+
+__device__ __forceinline__ void tc_store(const KsMacArgs& a, int z, int row, int comp, int l, int j, long long H,
+                                         long long Lo) {
+  // this lane holds B = H 2^32 + Lo for MAC row `row` (|H|, |Lo| < 2^56); lanes row^1 pair up
+  const int N = 1 << a.logN;
+  const size_t LN = (size_t)a.L * N;
+  const LimbConst& c = a.lcs.lc[l];
+  auto red = [&](long long h, long long lo) -> u64 {  // |h|, |lo| < 2^62
+    const u64 hu = (u64)(h + (long long)c.off62), lu = (u64)(lo + (long long)c.off62);
+    const u64 x = shoup_mul(hu, c.c32, c.c32_sh, c.q);
+    const u64 y = reduce_2q(lu, c.one_sh, c.q);
+    return csub(csub(x + y, c.two_q), c.q);
+  };
+  if (a.cn == 1) {
+    if (row < a.M) a.out[((size_t)(z * a.M + row) * 2 + comp) * LN + (size_t)l * N + j] = red(H, Lo);
+    return;
+  }
+  const long long H1 = __shfl_xor_sync(0xffffffffu, H, 1), L1 = __shfl_xor_sync(0xffffffffu, Lo, 1);
+  if ((row & 1) || row >= a.M) return;
+  const long long k = a.kscale;
+  // Walsh-Hadamard on the exact accumulators (Eq. 2): A0 = k (B0 + B1), A1 = B0 - B1
+  const u64 a0 = red(k * (H + H1), k * (Lo + L1));
+  const u64 a1 = red(H - H1, Lo - L1);
+  const u64 sg = __ldg(a.sign + (size_t)l * N + j), sgs = __ldg(a.sign + LN + (size_t)l * N + j);
+  u64 v = a0 + shoup_mul(a1, sg, sgs, c.q);
+  v = csub(csub(v, c.two_q), c.q);
+  a.out[((size_t)(z * (a.M / 2) + row / 2) * 2 + comp) * LN + (size_t)l * N + j] = v;
+}
+
+__global__ void __launch_bounds__(TC_THREADS, 1) mac_tc_kernel(KsMacArgs a, const u64* __restrict__ R,
+                                                               const int8_t* __restrict__ w8) {
+  __shared__ __align__(1024) uint8_t sA[TC_STAGES][4096];                 // 128 rows x 32 terms
+  __shared__ __align__(1024) uint8_t sB[TC_STAGES][8][TC_COLS * 32];      // 8 planes x 32 cols x 32 terms
+  __shared__ __align__(8) uint64_t full_bar[TC_STAGES], empty_bar[TC_STAGES], done_bar;
+  __shared__ uint32_t s_tmem;
+
+  const int N = 1 << a.logN;
+  const size_t LN = (size_t)a.L * N;
+  const int tiles = N / TC_POS;
+  const int l = blockIdx.x / tiles, j0 = (blockIdx.x % tiles) * TC_POS;
+  const int mt = blockIdx.y, z = blockIdx.z;
+  const int nmt = (a.Mpad + 127) / 128;
+  const int nchunks = a.Kpad / 32;
+  const int tid = threadIdx.x, warp = tid >> 5;
+
+  if (tid == 0) {
+    for (int s = 0; s < TC_STAGES; s++) {
+      mbar_init(&full_bar[s], 128);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "r"(TC_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+
+  if (tid < 128) {
+    // ---------------- producers: R chunk -> 8 byte planes; weights tile ----------------
+    const int n = tid & 31, kq = tid >> 5;           // column n (comp n/16, position n%16), terms 8kq..8kq+7
+    const int comp = n >> 4, pos = n & 15;
+    const u64* Rp = R + (size_t)z * a.K * 2 * LN + (size_t)comp * LN + (size_t)l * N + j0 + pos;
+    const int8_t* wsrc = w8 + ((size_t)(z % a.wblocks) * nmt + mt) * nchunks * 4096;
+    const int boff = (n >> 3) * 256 + (kq >> 1) * 128 + (n & 7) * 16 + (kq & 1) * 8;
+    for (int ch = 0; ch < nchunks; ch++) {
+      const int s = ch % TC_STAGES;
+      u64 x[8];
+#pragma unroll
+      for (int t = 0; t < 8; t++) {
+        const int kk = ch * 32 + kq * 8 + t;
+        x[t] = kk < a.K ? __ldg(Rp + (size_t)kk * 2 * LN) : 0ull;
+      }
+      const uint4 wa = __ldg(reinterpret_cast<const uint4*>(wsrc + (size_t)ch * 4096) + tid);
+      const uint4 wb = __ldg(reinterpret_cast<const uint4*>(wsrc + (size_t)ch * 4096) + 128 + tid);
+      if (ch >= TC_STAGES) mbar_wait(&empty_bar[s], ((ch / TC_STAGES) - 1) & 1);
+      reinterpret_cast<uint4*>(sA[s])[tid] = wa;
+      reinterpret_cast<uint4*>(sA[s])[128 + tid] = wb;
+      // byte transpose: plane b gets byte b of x[0..7] (8 consecutive terms of column n)
+#pragma unroll
+      for (int b = 0; b < 8; b++) {
+        uint32_t lo4[8];
+#pragma unroll
+        for (int t = 0; t < 8; t++) lo4[t] = (uint32_t)(x[t] >> (8 * b)) & 0xFFu;
+        const uint32_t w0 = lo4[0] | (lo4[1] << 8) | (lo4[2] << 16) | (lo4[3] << 24);
+        const uint32_t w1 = lo4[4] | (lo4[5] << 8) | (lo4[6] << 16) | (lo4[7] << 24);
+        *reinterpret_cast<uint2*>(&sB[s][b][boff]) = make_uint2(w0, w1);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&full_bar[s]);
+    }
+  } else if (tid == 128) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idesc = umma_idesc_s8u8(128, TC_COLS);
+    for (int ch = 0; ch < nchunks; ch++) {
+      const int s = ch % TC_STAGES;
+      mbar_wait(&full_bar[s], (ch / TC_STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t da = umma_desc_kmajor(smem_u32(sA[s]));
+#pragma unroll
+      for (int b = 0; b < 8; b++) {
+        const uint64_t db = umma_desc_kmajor(smem_u32(sB[s][b]));
+        const uint32_t acc = ch > 0;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (uint32_t)(b * TC_COLS)),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(&empty_bar[s]))
+                   : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(&done_bar))
+                 : "memory");
+  }
+
+  if (tid < 128) {
+    // ---------------- epilogue: lane = MAC row ----------------
+    mbar_wait(&done_bar, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int row = mt * 128 + warp * 32 + (tid & 31);
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+    for (int c0 = 0; c0 < TC_COLS; c0 += 8) {
+      uint32_t v[8][8];  // [plane][column]
+#pragma unroll
+      for (int b = 0; b < 8; b++) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(v[b][0]), "=r"(v[b][1]), "=r"(v[b][2]), "=r"(v[b][3]), "=r"(v[b][4]), "=r"(v[b][5]),
+                       "=r"(v[b][6]), "=r"(v[b][7])
+                     : "r"(lane_base + (uint32_t)(b * TC_COLS + c0)));
+      }
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int cc = 0; cc < 8; cc++) {
+        long long lo = 0, hi = 0;
+#pragma unroll
+        for (int b = 0; b < 4; b++) lo += (long long)(int32_t)v[b][cc] << (8 * b);
+#pragma unroll
+        for (int b = 4; b < 8; b++) hi += (long long)(int32_t)v[b][cc] << (8 * (b - 4));
+        const int col = c0 + cc;
+        tc_store(a, z, row, col >> 4, l, j0 + (col & 15), hi, lo);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS));
+}
+
+hy_status launch_mac_tc(const KsMacArgs& a, const u64* R, const int8_t* w8, int units, cudaStream_t s) {
+  const int N = 1 << a.logN;
+  dim3 grid((unsigned)(a.L * (N / TC_POS)), (unsigned)((a.Mpad + 127) / 128), (unsigned)units);
+  mac_tc_kernel<<<grid, TC_THREADS, 0, s>>>(a, R, w8);
+  HY_LAUNCH_CHECK();
+  return HY_OK;
+}
+
+template <int WM>
+hy_status launch_mac_gemm(const KsMacArgs& a, const u64* R, int units, cudaStream_t s) {
+  using TL = MgTile<WM>;
+  const int N = 1 << a.logN;
+  static bool attr_done = false;
+  if (!attr_done) {
+    HY_CUDA_TRY(cudaFuncSetAttribute(mac_gemm_kernel<WM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TL::SMEM));
+    attr_done = true;
+  }
+  dim3 grid((unsigned)(a.L * (N / TL::BNP)), (unsigned)(a.Mpad / TL::BM), (unsigned)units);
+  mac_gemm_kernel<WM><<<grid, 256, TL::SMEM, s>>>(a, R);
+  HY_LAUNCH_CHECK();
+  return HY_OK;
+}
+
+template <int LT>
+hy_status launch_permauto(const KsMacArgs& a, u64* R, int units, cudaStream_t s) {
+  const int N = 1 << a.logN;
+  dim3 grid((unsigned)((a.L * N + 255) / 256), (unsigned)a.T, (unsigned)units);
+  permauto_kernel<LT><<<grid, 256, 0, s>>>(a, R);
+  HY_LAUNCH_CHECK();
+  return HY_OK;
+}
+
 template <int WM, int LT>
 hy_status launch_ksmac_gemm(const KsMacArgs& a, int units, cudaStream_t s) {
   const int N = 1 << a.logN, BNP = 256 / WM, KC = 2 * WM;
@@ -734,7 +1180,23 @@ hy_status permdecomp(const hy_params* p, const u64* ct, size_t nct, u64* D, u64*
   return launch_fwd(p, j, nct * (p->L * p->L + p->L), s);
 }
 
-hy_status ksmac(const hy_weights* w, size_t nunits, cudaStream_t s) {
+// MAC-kernel timing (bench): record an event before/after each MAC launch when enabled
+static hy_status mac_mark(hy_weights* w, cudaStream_t s) {
+  if (!w->n_ev) return HY_OK;
+  if (!w->mac_ev) w->mac_ev = new std::vector<cudaEvent_t>();
+  std::vector<cudaEvent_t>& v = *w->mac_ev;
+  if (v.size() <= 2 * w->mac_launches + 1) {
+    cudaEvent_t e0, e1;
+    HY_CUDA_TRY(cudaEventCreate(&e0));
+    HY_CUDA_TRY(cudaEventCreate(&e1));
+    v.push_back(e0);
+    v.push_back(e1);
+  }
+  return HY_OK;
+}
+
+hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
+  w->mac_launches = 0;
   const hy_params* p = w->p;
   const hy_layout& lay = w->lay;
   const bool dw = w->shape.depthwise != 0;
@@ -760,11 +1222,49 @@ hy_status ksmac(const hy_weights* w, size_t nunits, cudaStream_t s) {
   a.lcs = limb_consts(p);
   const int units = (int)(dw ? nunits * lay.Jc : nunits);
   const int tile = hy_mac_tile(w->M);
-  switch (p->L) {  // key switching with a compile-time digit count for the common L
-    case 2: return launch_ksmac<2>(a, tile, units, s);
-    case 3: return launch_ksmac<3>(a, tile, units, s);
-    default: return launch_ksmac<0>(a, tile, units, s);
+  static const bool fused = getenv("HY_FUSED_KSMAC") != nullptr;  // A/B switches
+  static const bool fp64_mac = getenv("HY_MAC_FP64") != nullptr;
+  // depthwise, or M <= 32 MAC rows (C1, C2: latency-bound small layers): key switching fused into
+  // the FP64 MAC; dense M >= 64: PermAuto + tensor-core MAC
+  if (dw || tile < 8 || fused) {
+    HY_TRY(mac_mark(w, s));
+    if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[0], s));
+    hy_status st;
+    switch (p->L) {  // compile-time digit count for the common L
+      case 2: st = launch_ksmac<2>(a, tile, units, s); break;
+      case 3: st = launch_ksmac<3>(a, tile, units, s); break;
+      default: st = launch_ksmac<0>(a, tile, units, s); break;
+    }
+    HY_TRY(st);
+    if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[1], s));
+    w->mac_launches = 1;
+    return HY_OK;
   }
+  // dense: PermAuto materialises R for a batch of units, the MAC GEMM consumes it
+  const size_t LN = (size_t)p->L * p->N;
+  const int mrows = lay.cn == 2 ? w->M / 2 : w->M;  // output ciphertexts per unit
+  for (int u0 = 0; u0 < units; u0 += w->r_units) {
+    const int nb = std::min(w->r_units, units - u0);
+    KsMacArgs b = a;
+    b.D = a.D + (size_t)u0 * a.Jcb * p->L * LN;
+    b.C0 = a.C0 + (size_t)u0 * a.Jcb * LN;
+    b.out = a.out + (size_t)u0 * mrows * 2 * LN;
+    switch (p->L) {
+      case 2: HY_TRY(launch_permauto<2>(b, w->d_R, nb, s)); break;
+      case 3: HY_TRY(launch_permauto<3>(b, w->d_R, nb, s)); break;
+      case 5: HY_TRY(launch_permauto<5>(b, w->d_R, nb, s)); break;
+      default: HY_TRY(launch_permauto<0>(b, w->d_R, nb, s)); break;
+    }
+    HY_TRY(mac_mark(w, s));
+    if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[2 * w->mac_launches], s));
+    if (fp64_mac)
+      HY_TRY(launch_mac_gemm<8>(b, w->d_R, nb, s));
+    else
+      HY_TRY(launch_mac_tc(b, w->d_R, w->d_w8, nb, s));
+    if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[2 * w->mac_launches + 1], s));
+    w->mac_launches++;
+  }
+  return HY_OK;
 }
 
 hy_status finish_outputs(const hy_weights* w, size_t nunits, u64* ct_out, cudaStream_t s) {

@@ -16,7 +16,7 @@ __all__ = ["HyenaError", "hy_conv_shape", "hy_layout", "load_library", "library_
            "hy_plan_layout", "hy_params_create", "hy_params_destroy", "hy_keys_upload", "hy_encode_weights",
            "hy_weights_layout", "hy_weights_destroy", "hy_conv_eval", "hy_conv_eval_host", "hy_poly_mul",
            "hy_ntt_roundtrip", "hy_rotate", "hy_decrypt_debug", "hy_kernel_launches", "hy_weights_set_stage_events",
-           "layout_dict", "EXPORTED"]
+           "hy_weights_mac_time", "layout_dict", "EXPORTED"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 HY_MAX_TAPS = 49
@@ -26,7 +26,7 @@ HY_MAX_GALOIS = 64
 EXPORTED = ["hy_last_error", "hy_plan_layout", "hy_params_create", "hy_params_destroy", "hy_keys_upload",
             "hy_encode_weights", "hy_weights_layout", "hy_weights_destroy", "hy_conv_eval", "hy_conv_eval_host",
             "hy_poly_mul", "hy_ntt_roundtrip", "hy_rotate", "hy_decrypt_debug", "hy_kernel_launches",
-            "hy_weights_set_stage_events"]
+            "hy_weights_set_stage_events", "hy_weights_mac_time"]
 
 
 class HyenaError(RuntimeError):
@@ -89,6 +89,7 @@ def load_library() -> ctypes.CDLL:
         "hy_decrypt_debug": (i32, [vp, vp, vp, sz, u32, vp]),
         "hy_kernel_launches": (u64, []),
         "hy_weights_set_stage_events": (i32, [vp, vp, u32]),
+        "hy_weights_mac_time": (i32, [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(u32)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -230,3 +231,10 @@ def hy_weights_set_stage_events(w: int, events: Sequence) -> None:
             e.record()
     arr = (ctypes.c_void_p * max(1, len(events)))(*[int(e.cuda_event) for e in events])
     _check(load_library().hy_weights_set_stage_events(w, arr, len(events)), "hy_weights_set_stage_events")
+
+
+def hy_weights_mac_time(w: int):
+    """(summed device ms, launches) of the MAC kernel in the last hy_conv_eval (stage events set)."""
+    ms, n = ctypes.c_float(), ctypes.c_uint32()
+    _check(load_library().hy_weights_mac_time(w, ctypes.byref(ms), ctypes.byref(n)), "hy_weights_mac_time")
+    return float(ms.value), int(n.value)

@@ -75,12 +75,13 @@ for f in sorted(glob.glob("gpurun_out/prof_*_full.ncu-rep")):
             i = hdr.index(c)
             vals.append(f"{r[i]} {units[i]}".strip())
         out_md.append(f"| `{name[:60]}` | " + " | ".join(vals) + " |")
-        if "ksmac" in name:
+        if "mac" in name:
             i_r, i_w = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             b = float(r[i_r].replace(",", "")) * scale.get(units[i_r], 1) + \
                 float(r[i_w].replace(",", "")) * scale.get(units[i_w], 1)
-            traffic.setdefault(cfg, {})["ksmac"] = b
+            traffic.setdefault(cfg, {}).setdefault("mac", 0.0)
+            traffic[cfg]["mac"] = max(traffic[cfg]["mac"], b)
     os.system(f"cp {f} profiles/{tag}_{os.path.basename(f)[5:]}")
 if traffic:
     json.dump(traffic, open("profiles/traffic.json", "w"), indent=1)

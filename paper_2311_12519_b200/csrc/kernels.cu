@@ -423,18 +423,18 @@ __device__ __forceinline__ void ks_pair_regs(const u64* __restrict__ D, const u6
                                              const KeyRegs<LT>& k, int logN, int l, int jp, const LimbConst& c,
                                              u64& r0, u64& r1) {
   const size_t N = (size_t)1 << logN;
-  const u64 q = c.q, q2 = c.two_q;
+  const u64 q = c.q;
   u64 dv[LT];
 #pragma unroll
   for (int i = 0; i < LT; i++) dv[i] = __ldg(D + ((size_t)i * LT + l) * N + jp);
   u64 a0 = __ldg(C0 + (size_t)l * N + jp), a1 = 0;
 #pragma unroll
-  for (int i = 0; i < LT; i++) {
-    a0 = csub(a0 + shoup_mul(dv[i], k.v[2 * i], k.sh[2 * i], q), q2);
-    a1 = csub(a1 + shoup_mul(dv[i], k.v[2 * i + 1], k.sh[2 * i + 1], q), q2);
+  for (int i = 0; i < LT; i++) {  // lazy: < (2L + 1) q < 2^64, one reduction per component
+    a0 += shoup_mul(dv[i], k.v[2 * i], k.sh[2 * i], q);
+    a1 += shoup_mul(dv[i], k.v[2 * i + 1], k.sh[2 * i + 1], q);
   }
-  r0 = csub(a0, q);
-  r1 = csub(a1, q);
+  r0 = csub(reduce_2q(a0, c.one_sh, q), q);
+  r1 = csub(reduce_2q(a1, c.one_sh, q), q);
 }
 
 // generic (runtime L) version reading the key from global memory
@@ -486,6 +486,40 @@ __device__ __forceinline__ void r_value(const KsMacArgs& a, const u64* const* ke
   } else {
     ks_pair_any(D, C0, key, L, a.logN, l, j, jp, c, r0, r1);
   }
+}
+
+// Two-phase R value (prefetch the digit reads, key-switch later) for the tensor-core producers.
+template <int LT>
+struct RPre {
+  u64 c0, d[LT > 0 ? LT : 1];
+  int t;  // tap, -1 = padding term (R = 0)
+};
+
+template <int LT>
+__device__ __forceinline__ void r_finish(const KsMacArgs& a, const u64* const* keys, const RPre<LT>& pr, int l, int j,
+                                         const LimbConst& c, KeyRegs<LT>& kr, u64& r0, u64& r1) {
+  r0 = r1 = 0;
+  if (pr.t < 0) return;
+  const u64* key = keys[pr.t];
+  if (key == nullptr) {  // identity tap: (C0, D_{l,l})
+    r0 = pr.c0;
+    r1 = pr.d[0];
+    return;
+  }
+  if (kr.tau != pr.t || kr.pos != j) {
+    kr.load(key, a.logN, l, j);
+    kr.tau = pr.t;
+    kr.pos = j;
+  }
+  const u64 q = c.q, q2 = c.two_q;
+  u64 a0 = pr.c0, a1 = 0;
+#pragma unroll
+  for (int i = 0; i < LT; i++) {
+    a0 = csub(a0 + shoup_mul(pr.d[i], kr.v[2 * i], kr.sh[2 * i], q), q2);
+    a1 = csub(a1 + shoup_mul(pr.d[i], kr.v[2 * i + 1], kr.sh[2 * i + 1], q), q2);
+  }
+  r0 = csub(a0, q);
+  r1 = csub(a1, q);
 }
 
 __device__ __forceinline__ void store_outputs(const KsMacArgs& a, int z, int row, int comp, int l, int j,
@@ -707,15 +741,17 @@ __global__ void __launch_bounds__(256) permauto_kernel(KsMacArgs a, u64* __restr
 #pragma unroll
         for (int i = 0; i < LT; i++) dn[i] = __ldg(Dp + (size_t)(c + 1) * L * LN + (size_t)i * LN);
       }
-      const u64 q = cst.q, q2 = cst.two_q;
+      // lazy: each Shoup product is in [0, 2q); c0 + sum < (2L + 1) q < 2^64 for q < 2^60, L <= 7;
+      // one reduction per component
+      const u64 q = cst.q;
       u64 a0 = c0, a1 = 0;
 #pragma unroll
       for (int i = 0; i < LT; i++) {
-        a0 = csub(a0 + shoup_mul(d[i], kr.v[2 * i], kr.sh[2 * i], q), q2);
-        a1 = csub(a1 + shoup_mul(d[i], kr.v[2 * i + 1], kr.sh[2 * i + 1], q), q2);
+        a0 += shoup_mul(d[i], kr.v[2 * i], kr.sh[2 * i], q);
+        a1 += shoup_mul(d[i], kr.v[2 * i + 1], kr.sh[2 * i + 1], q);
       }
-      __stcs(out + (size_t)c * 2 * LN, csub(a0, q));
-      __stcs(out + (size_t)c * 2 * LN + LN, csub(a1, q));
+      __stcs(out + (size_t)c * 2 * LN, csub(reduce_2q(a0, cst.one_sh, q), q));
+      __stcs(out + (size_t)c * 2 * LN + LN, csub(reduce_2q(a1, cst.one_sh, q), q));
     }
   } else {
     for (int c = 0; c < a.Jcb; c++) {
@@ -941,6 +977,16 @@ __device__ __forceinline__ void tc_store(const KsMacArgs& a, int z, int row, int
   a.out[((size_t)(z * (a.M / 2) + row / 2) * 2 + comp) * LN + (size_t)l * N + j] = v;
 }
 
+// 4x4 byte transpose: w[b] = byte b of x[0], x[1], x[2], x[3]
+__device__ __forceinline__ void byte_tr4(const uint32_t* x, uint32_t* w) {
+  const uint32_t t0 = __byte_perm(x[0], x[1], 0x5140), t1 = __byte_perm(x[0], x[1], 0x7362);
+  const uint32_t t2 = __byte_perm(x[2], x[3], 0x5140), t3 = __byte_perm(x[2], x[3], 0x7362);
+  w[0] = __byte_perm(t0, t2, 0x5410);
+  w[1] = __byte_perm(t0, t2, 0x7632);
+  w[2] = __byte_perm(t1, t3, 0x5410);
+  w[3] = __byte_perm(t1, t3, 0x7632);
+}
+
 __global__ void __launch_bounds__(TC_THREADS, 1) mac_tc_kernel(KsMacArgs a, const u64* __restrict__ R,
                                                                const int8_t* __restrict__ w8) {
   __shared__ __align__(1024) uint8_t sA[TC_STAGES][4096];                 // 128 rows x 32 terms
@@ -982,29 +1028,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mac_tc_kernel(KsMacArgs a, cons
     const u64* Rp = R + (size_t)z * a.K * 2 * LN + (size_t)comp * LN + (size_t)l * N + j0 + pos;
     const int8_t* wsrc = w8 + ((size_t)(z % a.wblocks) * nmt + mt) * nchunks * 4096;
     const int boff = (n >> 3) * 256 + (kq >> 1) * 128 + (n & 7) * 16 + (kq & 1) * 8;
+    u64 xn[8];  // the next chunk's R values, in flight while the current one is transposed
+#pragma unroll
+    for (int t = 0; t < 8; t++) {
+      const int kk = kq * 8 + t;
+      xn[t] = kk < a.K ? __ldcs(Rp + (size_t)kk * 2 * LN) : 0ull;
+    }
     for (int ch = 0; ch < nchunks; ch++) {
       const int s = ch % TC_STAGES;
       u64 x[8];
 #pragma unroll
       for (int t = 0; t < 8; t++) {
-        const int kk = ch * 32 + kq * 8 + t;
-        x[t] = kk < a.K ? __ldg(Rp + (size_t)kk * 2 * LN) : 0ull;
+        x[t] = xn[t];
+        const int kk = (ch + 1) * 32 + kq * 8 + t;
+        xn[t] = kk < a.K ? __ldcs(Rp + (size_t)kk * 2 * LN) : 0ull;
       }
       const uint4 wa = __ldg(reinterpret_cast<const uint4*>(wsrc + (size_t)ch * 4096) + tid);
       const uint4 wb = __ldg(reinterpret_cast<const uint4*>(wsrc + (size_t)ch * 4096) + 128 + tid);
       if (ch >= TC_STAGES) mbar_wait(&empty_bar[s], ((ch / TC_STAGES) - 1) & 1);
       reinterpret_cast<uint4*>(sA[s])[tid] = wa;
       reinterpret_cast<uint4*>(sA[s])[128 + tid] = wb;
-      // byte transpose: plane b gets byte b of x[0..7] (8 consecutive terms of column n)
-#pragma unroll
-      for (int b = 0; b < 8; b++) {
-        uint32_t lo4[8];
-#pragma unroll
-        for (int t = 0; t < 8; t++) lo4[t] = (uint32_t)(x[t] >> (8 * b)) & 0xFFu;
-        const uint32_t w0 = lo4[0] | (lo4[1] << 8) | (lo4[2] << 16) | (lo4[3] << 24);
-        const uint32_t w1 = lo4[4] | (lo4[5] << 8) | (lo4[6] << 16) | (lo4[7] << 24);
-        *reinterpret_cast<uint2*>(&sB[s][b][boff]) = make_uint2(w0, w1);
+      // byte transpose (PRMT): plane b gets byte b of x[0..7] (8 consecutive terms of column n)
+      uint32_t pa[8], pb[8];
+      {
+        const uint32_t l0[4] = {(uint32_t)x[0], (uint32_t)x[1], (uint32_t)x[2], (uint32_t)x[3]};
+        const uint32_t h0[4] = {(uint32_t)(x[0] >> 32), (uint32_t)(x[1] >> 32), (uint32_t)(x[2] >> 32),
+                                (uint32_t)(x[3] >> 32)};
+        const uint32_t l1[4] = {(uint32_t)x[4], (uint32_t)x[5], (uint32_t)x[6], (uint32_t)x[7]};
+        const uint32_t h1[4] = {(uint32_t)(x[4] >> 32), (uint32_t)(x[5] >> 32), (uint32_t)(x[6] >> 32),
+                                (uint32_t)(x[7] >> 32)};
+        byte_tr4(l0, pa);
+        byte_tr4(h0, pa + 4);
+        byte_tr4(l1, pb);
+        byte_tr4(h1, pb + 4);
       }
+#pragma unroll
+      for (int b = 0; b < 8; b++) *reinterpret_cast<uint2*>(&sB[s][b][boff]) = make_uint2(pa[b], pb[b]);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&full_bar[s]);
     }
@@ -1066,6 +1125,195 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mac_tc_kernel(KsMacArgs a, cons
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS));
+}
+
+// Fused variant: the producer warps compute the key-switched R values themselves (no R in
+// HBM): per chunk of 32 terms each producer thread key-switches 4 consecutive terms of one
+// position (tap keys cached in registers, the next chunk's digit reads already in flight) and
+// byte-transposes the 4 (c0, c1) pairs into the 8 planes with PRMT.
+template <int LT>
+__global__ void __launch_bounds__(TC_THREADS, 1) ksmac_tc_kernel(KsMacArgs a, const int8_t* __restrict__ w8) {
+  __shared__ __align__(1024) uint8_t sA[TC_STAGES][4096];
+  __shared__ __align__(1024) uint8_t sB[TC_STAGES][8][TC_COLS * 32];
+  __shared__ __align__(8) uint64_t full_bar[TC_STAGES], empty_bar[TC_STAGES], done_bar;
+  __shared__ uint32_t s_tmem;
+  __shared__ const u64* s_key[HY_MAX_TAPS];
+  __shared__ GaloisAct s_act[HY_MAX_TAPS];
+
+  const int N = 1 << a.logN;
+  const size_t LN = (size_t)LT * N;
+  const int tiles = N / TC_POS;
+  const int l = blockIdx.x / tiles, j0 = (blockIdx.x % tiles) * TC_POS;
+  const int mt = blockIdx.y, z = blockIdx.z;
+  const int nmt = (a.Mpad + 127) / 128;
+  const int nchunks = a.Kpad / 32;
+  const int tid = threadIdx.x, warp = tid >> 5;
+
+  for (int t = tid; t < a.T; t += TC_THREADS) {
+    s_key[t] = a.keys[t];
+    s_act[t] = a.act[t];
+  }
+  if (tid == 0) {
+    for (int s = 0; s < TC_STAGES; s++) {
+      mbar_init(&full_bar[s], 128);
+      mbar_init(&empty_bar[s], 1);
+    }
+    mbar_init(&done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "r"(TC_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+
+  if (tid < 128) {
+    // ---------------- producers ----------------
+    const int pos = tid & 15, kg = tid >> 4;  // position, terms 4kg .. 4kg+3 of each chunk
+    const int j = j0 + pos;
+    const LimbConst cst = a.lcs.lc[l];
+    const int8_t* wsrc = w8 + ((size_t)(z % a.wblocks) * nmt + mt) * nchunks * 4096;
+    const u64* C0u = a.C0 + (size_t)z * a.Jcb * LN + (size_t)l * N;
+    const u64* Du = a.D + (size_t)z * a.Jcb * LT * LN + (size_t)l * N;
+    // plane byte offsets (K-major canonical) of column pos (c0) and 16 + pos (c1), terms 4kg..4kg+3
+    const int off0 = (pos >> 3) * 256 + (kg >> 2) * 128 + (pos & 7) * 16 + (kg & 3) * 4;
+    const int off1 = off0 + 2 * 256;
+    KeyRegs<LT> kr;
+    RPre<LT> pre[4];
+    auto load_chunk = [&](int ch, RPre<LT>* pr) {
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        const int kk = ch * 32 + kg * 4 + t;
+        pr[t].t = -1;
+        if (kk >= a.K) continue;
+        const int tap = kk / a.Jcb, c = kk - tap * a.Jcb;
+        pr[t].t = tap;
+        const u64* C0 = C0u + (size_t)c * LN;
+        const u64* D = Du + (size_t)c * LT * LN;
+        if (s_key[tap] == nullptr) {
+          pr[t].c0 = __ldg(C0 + j);
+          pr[t].d[0] = __ldg(D + (size_t)l * LN + j);
+        } else {
+          const int jp = galois_perm(j, s_act[tap], N >> 1);
+          pr[t].c0 = __ldg(C0 + jp);
+#pragma unroll
+          for (int i = 0; i < LT; i++) pr[t].d[i] = __ldg(D + (size_t)i * LN + jp);
+        }
+      }
+    };
+    load_chunk(0, pre);
+    for (int ch = 0; ch < nchunks; ch++) {
+      const int s = ch % TC_STAGES;
+      RPre<LT> cur[4];
+#pragma unroll
+      for (int t = 0; t < 4; t++) cur[t] = pre[t];
+      if (ch + 1 < nchunks) load_chunk(ch + 1, pre);
+      const uint4 wa = __ldg(reinterpret_cast<const uint4*>(wsrc + (size_t)ch * 4096) + tid);
+      const uint4 wb = __ldg(reinterpret_cast<const uint4*>(wsrc + (size_t)ch * 4096) + 128 + tid);
+      uint32_t lo0[4], hi0[4], lo1[4], hi1[4];
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        u64 r0, r1;
+        r_finish<LT>(a, s_key, cur[t], l, j, cst, kr, r0, r1);
+        lo0[t] = (uint32_t)r0;
+        hi0[t] = (uint32_t)(r0 >> 32);
+        lo1[t] = (uint32_t)r1;
+        hi1[t] = (uint32_t)(r1 >> 32);
+      }
+      // 4x4 byte transposes: word b of plane b holds byte b of the 4 terms
+      auto tr4 = [](const uint32_t* x, uint32_t* w) {
+        const uint32_t t0 = __byte_perm(x[0], x[1], 0x5140), t1 = __byte_perm(x[0], x[1], 0x7362);
+        const uint32_t t2 = __byte_perm(x[2], x[3], 0x5140), t3 = __byte_perm(x[2], x[3], 0x7362);
+        w[0] = __byte_perm(t0, t2, 0x5410);
+        w[1] = __byte_perm(t0, t2, 0x7632);
+        w[2] = __byte_perm(t1, t3, 0x5410);
+        w[3] = __byte_perm(t1, t3, 0x7632);
+      };
+      uint32_t p0[8], p1[8];
+      tr4(lo0, p0);
+      tr4(hi0, p0 + 4);
+      tr4(lo1, p1);
+      tr4(hi1, p1 + 4);
+      if (ch >= TC_STAGES) mbar_wait(&empty_bar[s], ((ch / TC_STAGES) - 1) & 1);
+      reinterpret_cast<uint4*>(sA[s])[tid] = wa;
+      reinterpret_cast<uint4*>(sA[s])[128 + tid] = wb;
+#pragma unroll
+      for (int b = 0; b < 8; b++) {
+        *reinterpret_cast<uint32_t*>(&sB[s][b][off0]) = p0[b];
+        *reinterpret_cast<uint32_t*>(&sB[s][b][off1]) = p1[b];
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&full_bar[s]);
+    }
+  } else if (tid == 128) {
+    const uint32_t idesc = umma_idesc_s8u8(128, TC_COLS);
+    for (int ch = 0; ch < nchunks; ch++) {
+      const int s = ch % TC_STAGES;
+      mbar_wait(&full_bar[s], (ch / TC_STAGES) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint64_t da = umma_desc_kmajor(smem_u32(sA[s]));
+#pragma unroll
+      for (int b = 0; b < 8; b++) {
+        const uint64_t db = umma_desc_kmajor(smem_u32(sB[s][b]));
+        const uint32_t acc = ch > 0;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (uint32_t)(b * TC_COLS)),
+            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(&empty_bar[s]))
+                   : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(&done_bar))
+                 : "memory");
+  }
+
+  if (tid < 128) {
+    mbar_wait(&done_bar, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int row = mt * 128 + warp * 32 + (tid & 31);
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+    for (int c0 = 0; c0 < TC_COLS; c0 += 8) {
+      uint32_t v[8][8];
+#pragma unroll
+      for (int b = 0; b < 8; b++) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(v[b][0]), "=r"(v[b][1]), "=r"(v[b][2]), "=r"(v[b][3]), "=r"(v[b][4]), "=r"(v[b][5]),
+                       "=r"(v[b][6]), "=r"(v[b][7])
+                     : "r"(lane_base + (uint32_t)(b * TC_COLS + c0)));
+      }
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int cc = 0; cc < 8; cc++) {
+        long long lo = 0, hi = 0;
+#pragma unroll
+        for (int b = 0; b < 4; b++) lo += (long long)(int32_t)v[b][cc] << (8 * b);
+#pragma unroll
+        for (int b = 4; b < 8; b++) hi += (long long)(int32_t)v[b][cc] << (8 * (b - 4));
+        const int col = c0 + cc;
+        tc_store(a, z, row, col >> 4, l, j0 + (col & 15), hi, lo);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS));
+}
+
+template <int LT>
+hy_status launch_ksmac_tc(const KsMacArgs& a, const int8_t* w8, int units, cudaStream_t s) {
+  const int N = 1 << a.logN;
+  dim3 grid((unsigned)(a.L * (N / TC_POS)), (unsigned)((a.Mpad + 127) / 128), (unsigned)units);
+  ksmac_tc_kernel<LT><<<grid, TC_THREADS, 0, s>>>(a, w8);
+  HY_LAUNCH_CHECK();
+  return HY_OK;
 }
 
 hy_status launch_mac_tc(const KsMacArgs& a, const u64* R, const int8_t* w8, int units, cudaStream_t s) {
@@ -1235,6 +1483,18 @@ hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
       case 3: st = launch_ksmac<3>(a, tile, units, s); break;
       default: st = launch_ksmac<0>(a, tile, units, s); break;
     }
+    HY_TRY(st);
+    if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[1], s));
+    w->mac_launches = 1;
+    return HY_OK;
+  }
+  static const bool fused_tc = getenv("HY_FUSED_TC") != nullptr && !fp64_mac;  // experimental (slower)
+  if (fused_tc && (p->L == 2 || p->L == 3 || p->L == 5)) {  // fused key switching + tensor-core MAC
+    HY_TRY(mac_mark(w, s));
+    if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[0], s));
+    hy_status st = p->L == 2 ? launch_ksmac_tc<2>(a, w->d_w8, units, s)
+                 : p->L == 3 ? launch_ksmac_tc<3>(a, w->d_w8, units, s)
+                             : launch_ksmac_tc<5>(a, w->d_w8, units, s);
     HY_TRY(st);
     if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[1], s));
     w->mac_launches = 1;

@@ -79,6 +79,15 @@ CASES = {
     "k5x5": dict(N=2048, bits=50, L=2, batch=1, Ci=2, Co=2, H=8, W=8, kh=5, kw=5, pad=2),
     "wide_weights": dict(N=2048, bits=60, L=3, batch=1, Ci=8, Co=8, H=6, W=6, kh=3, kw=3, pad=1,
                          xrange=(-128, 128), wrange=(-128, 128)),
+    # >= 64 MAC rows: the tensor-core MAC path (tcgen05 kind::i8), with row padding to 128
+    "tc_cn2_rows140": dict(N=1024, bits=50, L=2, batch=5, Ci=3, Co=70, H=6, W=6, kh=3, kw=3, pad=1,
+                           xrange=(-128, 128), wrange=(-128, 128)),
+    "tc_cn1_units": dict(N=1024, bits=50, L=3, batch=17, Ci=3, Co=70, H=6, W=6, kh=3, kw=3, pad=1,
+                         xrange=(-128, 128), wrange=(-128, 128)),
+    "tc_cn2": dict(N=2048, bits=60, L=3, batch=1, Ci=5, Co=34, H=6, W=6, kh=3, kw=3, pad=1,
+                   xrange=(-128, 128), wrange=(-128, 128)),
+    "tc_cn2_L5_rows130": dict(N=1024, bits=50, L=5, batch=2, Ci=2, Co=65, H=5, W=5, kh=3, kw=3, pad=1),
+    "tc_pw_cn1": dict(N=1024, bits=50, L=3, batch=9, Ci=40, Co=66, H=6, W=6, kh=1, kw=1, pad=0),
 }
 
 

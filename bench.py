@@ -155,7 +155,11 @@ def run_gpu(args, cfg, rank, world):
             shard_mod.gather_outputs(ct_out, shard, full.Jout)
 
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    mac_path = None
     if w is not None:
+        if args.mac_path:
+            hy.hy_weights_set_mac_path(w, args.mac_path)
+        mac_path = hy.hy_weights_mac_path(w)
         hy.hy_weights_set_stage_events(w, ev)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(args.warmup):
@@ -219,7 +223,7 @@ def run_gpu(args, cfg, rank, world):
     if w is not None:
         hy.hy_weights_destroy(w)
     hy.hy_params_destroy(p)
-    return dict(total_ms=total_ms, step_ms=step_ms,
+    return dict(total_ms=total_ms, step_ms=step_ms, mac_path=mac_path,
                 stage_ms=[statistics.mean(s) if s else 0.0 for s in stage_ms],
                 mac_ms=statistics.mean(mac_ms) if mac_ms else 0.0, mac_launches=mac_n,
                 launches=launches, clocks=clk.summary(), lay=lay, full=full, e2e_s=e2e_s, e2e_steps=e2e_steps,
@@ -227,10 +231,14 @@ def run_gpu(args, cfg, rank, world):
 
 
 def layer_work(cfg, lay):
-    """Algorithmic work of one hy_conv_eval on layout `lay`:
-    coefficient-MACs of the fused S2+S3 kernel (M MAC rows x K terms x 2LN columns per unit;
-    c_n = 2 has 4 rows per output ct = 2 diagonals x 2 slot rows), 2 exact
-    DFMA each (30-bit halves); hoisted rotations; row swaps."""
+    """Algorithmic work of one hy_conv_eval on layout `lay`.
+    coef_macs: coefficient-MACs of S3 (M MAC rows x K terms x 2LN columns per unit; c_n = 2 has
+    4 rows per output ct = 2 diagonals x 2 slot rows).  Modular products
+    ("modmul" = one 64-bit Shoup product, the unit of the INT roofline) per stage:
+      S1: (L^2 + L) forward NTTs per input ct, N/2 log2 N butterflies each;
+      S2: 2 L^2 N key-switching products per (input ct, non-identity tap) (hoisted PermAuto);
+      S4+S5: c_n = 2 non-depthwise: per output ct L INTT + L(L-1) NTT + 2 L^2 N key switching +
+             2L INTT (row swap, then coefficient form); otherwise 2L INTT per output ct."""
     L, N, T = len(cfg.primes), cfg.N, lay.n_taps
     ctw = 2 * L * N
     if cfg.depthwise:
@@ -238,9 +246,16 @@ def layer_work(cfg, lay):
     else:
         M, K, units = (4 * lay.Jo if lay.cn == 2 else lay.Jo), lay.Jc * T, lay.U
     mac = M * K * ctw * units
-    rot = lay.J * sum(1 for s in lay.tap_step[:T] if s % (N // 2))
+    ntap = sum(1 for s in lay.tap_step[:T] if s % (N // 2))
+    rot = lay.J * ntap
     swaps = lay.Jout if (lay.cn == 2 and not cfg.depthwise) else 0
-    return dict(coef_macs=mac, dfma=2 * mac, rotations=rot, rowswaps=swaps, M=M, K=K, units=units)
+    bfly = N // 2 * int(np.log2(N))
+    s1 = lay.J * (L * L + L) * bfly
+    s2 = rot * 2 * L * L * N
+    s45 = swaps * ((L + L * (L - 1)) * bfly + 2 * L * L * N) + lay.Jout * 2 * L * bfly
+    return dict(coef_macs=mac, dfma=2 * mac, rotations=rot, rowswaps=swaps, M=M, K=K, units=units,
+                modmul={"S1_permdecomp": s1, "S2S3_ksmac_wht": s2, "S4S5_align_intt": s45},
+                r_bytes=K * ctw * 8 * units, in_bytes=lay.J * ctw * 8, out_bytes=lay.Jout * ctw * 8)
 
 
 def traffic_for(cfg_name, kernel):
@@ -251,31 +266,65 @@ def traffic_for(cfg_name, kernel):
         return None
 
 
+MODMUL_PER_CLK_SM = 4.0   # 64-bit Shoup product = 6 IMAD.WIDE (2 issue slots) + 4 IMAD on 64 lanes/clk/SM
+I8_PER_BF16 = 2.0         # dense int8 / bf16 tensor throughput, nominal (B200_PROFILING.md: 4.5 vs 2.25 P)
+MAC_KERNEL = {"thin": "ksmac_thin_kernel (fused S2+S3, FP64 MAC)",
+              "tc_fused": "ksmac_tc_kernel (fused S2+S3: key switching + tcgen05 int8 MAC)",
+              "tc_split": "mac_tc_kernel (S3 tcgen05 int8 MAC over stored R)",
+              "fp64_fused": "ksmac_gemm_kernel (fused S2+S3, FP64 MAC)",
+              "fp64_split": "mac_gemm_kernel (S3 FP64 MAC over stored R)"}
+
+
 def roofline(cfg, res, peaks, steps):
-    """Roofline of the MAC kernel (S3: the exact lazy MAC + WHT + reduction + sign PMult; the
-    dominant kernel of every dense config), timed per launch by library-owned CUDA events on its
-    stream: bound by the FP64 pipe that carries the MAC (2 DFMA per coefficient-MAC).  Peak =
-    64 DFMA/clk/SM x 148 SMs x the max SM clock (derived).  Depthwise layers fuse
-    the key switching into a thin MAC and are bound by it (int pipes / L2): reported against the
-    same FP64 peak for comparability."""
+    """Roofline of the dominant kernel of the step.  Stage times come from CUDA events
+    the library records on its stream; the MAC kernel's own launches are timed separately.
+      - INT-bound kernels (NTTs, key switching fused into the MAC): achieved = algorithmic 64-bit
+        modular products / time; peak = MODMUL_PER_CLK_SM x 148 SMs x max SM clock (unit count
+        derived in DESIGN.md §4, measured by tools/intbench).
+      - tc_split MAC: HBM-bound streaming of the stored rotated inputs R (algorithmic bytes = R read
+        + outputs written) against the measured HBM copy bandwidth.
+      - FP64 MAC variants: 2 exact DFMA per coefficient-MAC against 64 DFMA/clk/SM."""
     lay = res["lay"]
     w = layer_work(cfg, lay)
-    st = res["stage_ms"]
+    st = dict(zip(STAGES, res["stage_ms"]))
+    path = res.get("mac_path", "tc_fused")
     clk_mhz = res["clocks"].get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
-    kms = res["mac_ms"] or st[1]
-    achieved = w["dfma"] / (kms * 1e-3) / 1e12
-    peak = DFMA_PER_CLK_SM * SM_COUNT * clk_mhz * 1e6 / 1e12
-    dom = STAGES[int(np.argmax(st))]
+    int_peak = MODMUL_PER_CLK_SM * SM_COUNT * clk_mhz * 1e6 / 1e9          # Gmodmul/s
+    mac_ms = res["mac_ms"] or st["S2S3_ksmac_wht"]
     per_step = max(1, res["mac_launches"] // max(1, steps))
-    name = ("ksmac_thin_kernel (fused S2+S3)" if cfg.depthwise else
-            "mac_gemm_kernel (S3)" if per_step > 0 and kms < st[1] * 0.999 else "ksmac_gemm_kernel (fused S2+S3)")
-    return {"kernel": name,
-            "bound": "alu", "achieved": achieved, "peak": peak, "unit": "TDFMA/s", "frac": achieved / peak,
-            "traffic": traffic_for(cfg.name, "mac"),
-            "kernel_ms_per_step": kms, "launches_per_step": per_step, "share_of_step": kms / max(1e-9, sum(st)),
-            "dominant_stage": dom,
-            "peak_note": f"FP64 pipe {DFMA_PER_CLK_SM}/clk/SM x {SM_COUNT} SMs x {clk_mhz:.0f} MHz (derived from "
-                         "the guide's unit counts; DESIGN.md §6)"}
+    dom = max(st, key=st.get)
+    kernels = {}
+    for stage in ("S1_permdecomp", "S4S5_align_intt"):
+        a = w["modmul"][stage] / (st[stage] * 1e-3) / 1e9 if st[stage] > 0 else 0.0
+        kernels[stage] = {"bound": "alu", "achieved": a, "peak": int_peak, "unit": "Gmodmul/s",
+                          "frac": a / int_peak, "ms": st[stage]}
+    if path in ("tc_fused", "thin"):
+        a = w["modmul"]["S2S3_ksmac_wht"] / (mac_ms * 1e-3) / 1e9
+        mac = {"bound": "alu", "achieved": a, "peak": int_peak, "unit": "Gmodmul/s", "frac": a / int_peak}
+    elif path == "tc_split":
+        hbm = peaks.get("hbm_gbs", 6546.6)
+        a = (w["r_bytes"] + w["out_bytes"] * (2 if lay.cn == 2 and not cfg.depthwise else 1)) / (mac_ms * 1e-3) / 1e9
+        mac = {"bound": "hbm", "achieved": a, "peak": hbm, "unit": "GB/s", "frac": a / hbm}
+    else:
+        pk = DFMA_PER_CLK_SM * SM_COUNT * clk_mhz * 1e6 / 1e12
+        a = w["dfma"] / (mac_ms * 1e-3) / 1e12
+        mac = {"bound": "alu", "achieved": a, "peak": pk, "unit": "TDFMA/s", "frac": a / pk}
+    mac.update(kernel=MAC_KERNEL[path], ms=mac_ms, launches_per_step=per_step)
+    if path.startswith("tc"):
+        i8 = 2 * 8 * w["coef_macs"] / (mac_ms * 1e-3) / 1e12                # 8 byte planes
+        i8_peak = peaks.get("bf16_tflops", 2250.0) * I8_PER_BF16
+        mac["tensor_int8"] = {"achieved": i8, "peak": i8_peak, "unit": "TOP/s", "frac": i8 / i8_peak}
+    kernels["S2S3_ksmac_wht"] = mac
+    top = dict(kernels[dom])
+    top.setdefault("kernel", {"S1_permdecomp": "ntt_fwd_kernel<PermDecompJob> (S1)",
+                              "S4S5_align_intt": "S4+S5 stage (row-swap key switching, NTT/INTT)"}.get(dom, dom))
+    top["dominant_stage"] = dom
+    top["share_of_step"] = st[dom] / max(1e-9, sum(st.values()))
+    top["traffic"] = traffic_for(cfg.name, dom)
+    top["peak_note"] = (f"INT: {MODMUL_PER_CLK_SM:g} Shoup modmul/clk/SM x {SM_COUNT} SMs x {clk_mhz:.0f} MHz (derived "
+                        "from the unit counts, DESIGN.md §4); HBM: MEASURED_PEAKS.json hbm_gbs")
+    top["stages"] = kernels
+    return top
 
 
 # --------------------------------------------------------------------------------------------
@@ -356,6 +405,7 @@ def main():
     ap.add_argument("--impl", default="hyena", choices=["hyena", "reference"])
     ap.add_argument("--mode", default="replica", choices=["replica", "shard"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mac-path", default=None, help="A/B: force an S2+S3 kernel path (hyena.MAC_PATHS)")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"
     cfg = synth.configs()[args.config]
@@ -395,6 +445,7 @@ def main():
                                        else f"replica x{world} (independent images per GPU)")},
             "ct_mac_gops": layers_s * work["coef_macs"] / 1e9,
             "stages_ms": dict(zip(STAGES, res["stage_ms"])),
+            "mac_path": res["mac_path"],
             "roofline": roofline(cfg, res, peaks, args.steps) if lay is not None else None,
             "gpu_launches": res["launches"],
             "clocks": res["clocks"],

@@ -159,6 +159,19 @@ hy_status hy_weights_set_stage_events(hy_weights* w, void* const* events, uint32
  * the last one).  Errors: HY_EINVAL, HY_ECUDA. */
 hy_status hy_weights_mac_time(const hy_weights* w, float* total_ms, uint32_t* launches);
 
+/* Kernel choice for S2 + S3, fixed by hy_encode_weights from the layout:
+ *   0 HY_MAC_THIN        depthwise: key switching fused into a thin FP64 MAC;
+ *   1 HY_MAC_TC_FUSED    dense, M <= 128 MAC rows, L in {2,3,5}: key switching in the producer
+ *                        warps of the tcgen05 int8 MAC (rotated inputs never stored);
+ *   2 HY_MAC_TC_SPLIT    dense: PermAuto materialises the rotated inputs, tcgen05 MAC reads them;
+ *   3 HY_MAC_FP64_FUSED  dense, M <= 32: key switching + FP64 DFMA MAC (30-bit halves);
+ *   4 HY_MAC_FP64_SPLIT  dense, M > 32: PermAuto + FP64 DFMA MAC.
+ * Every path computes the same bits (the MAC is exact integer arithmetic).  set_mac_path selects
+ * another valid path for A/B measurement and parity tests (allocates the rotated-input workspace
+ * of the split paths).  Errors: HY_EINVAL (path not valid for this layout), HY_ENOMEM. */
+hy_status hy_weights_mac_path(const hy_weights* w, int32_t* path);
+hy_status hy_weights_set_mac_path(hy_weights* w, int32_t path);
+
 /* Debug decryption (PAPER.md:256-267 [\ignore]): for each of n device ciphertexts
  * [n][2][L][N] computes [c0 + c1 s]_{q_l} on the GPU, then on the host the exact CRT
  * rounding m = [round(t x / Q)]_t, slot decoding and multiplication by

@@ -431,6 +431,7 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
     w->wblocks = 1;
   }
   w->Mpad = hy_mac_mpad(w->M);
+  w->mac_path = hy_mac_path(w->M, (int)p->L, dw);
   w->Kpad = (w->K + 31) / 32 * 32;  // multiple of the MAC K chunks (16 FP64 GEMM, 32 tcgen05)
   // weight table (S0), [block][kk][row] as exact doubles; row semantics documented in DESIGN.md §4
   std::vector<double> wt((size_t)w->wblocks * w->Kpad * w->Mpad, 0.0);
@@ -472,6 +473,12 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
               (int8_t)wt[((size_t)b * w->Kpad + kk) * w->Mpad + row];
         }
     st = upload((void**)&w->d_w8, w8.data(), w8.size());
+  }
+  if (st == HY_OK) {
+    std::vector<int32_t> kt((size_t)(w->Kpad + 63) / 64 * 64, -1);
+    const int Jcb = dw ? 1 : (int)lay.Jc;
+    for (int kk = 0; kk < w->K; kk++) kt[kk] = ((kk / Jcb) << 16) | (kk % Jcb);
+    st = upload((void**)&w->d_kt, kt.data(), kt.size() * sizeof(int32_t));
   }
   if (st != HY_OK) {
     hy_weights_destroy(w);
@@ -520,7 +527,8 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
       {&w->d_P, Jo * ctw * ((lay.cn == 2 && !dw) ? 2 : 1)},
       {&w->d_D2, (lay.cn == 2 && !dw) ? Jo * L * L * N + Jo * L * N : 0},
       {&w->d_X, (lay.cn == 2 && !dw) ? Jo * ctw : 0},
-      {&w->d_R, !dw ? (size_t)w->r_units * w->K * ctw : 0},
+      {&w->d_R, (w->mac_path == HY_MAC_TC_SPLIT || w->mac_path == HY_MAC_FP64_SPLIT)
+                    ? (size_t)w->r_units * w->K * ctw : 0},
       {&w->d_in, Jin * ctw},
       {&w->d_out, Jo * ctw},
   };
@@ -563,6 +571,41 @@ extern "C" hy_status hy_weights_mac_time(const hy_weights* w, float* total_ms, u
   return HY_OK;
 }
 
+extern "C" hy_status hy_weights_mac_path(const hy_weights* w, int32_t* path) {
+  HY_CHECK(w && path, HY_EINVAL, "null argument");
+  *path = w->mac_path;
+  return HY_OK;
+}
+
+extern "C" hy_status hy_weights_set_mac_path(hy_weights* w, int32_t path) {
+  HY_CHECK(w, HY_EINVAL, "null argument");
+  const bool dw = w->shape.depthwise != 0;
+  const int L = (int)w->p->L;
+  bool ok = false;
+  switch (path) {
+    case HY_MAC_THIN: ok = dw; break;
+    case HY_MAC_TC_FUSED: ok = !dw && w->M <= 128 && (L == 2 || L == 3 || L == 5); break;
+    case HY_MAC_TC_SPLIT: ok = !dw; break;
+    case HY_MAC_FP64_SPLIT: ok = !dw && w->M > 32; break;  // 64-row FP64 tiles (hy_mac_mpad)
+    case HY_MAC_FP64_FUSED: ok = !dw && w->M <= 32; break;
+  }
+  HY_CHECK(ok, HY_EINVAL, "MAC path %d is not valid for this layout (M = %d, L = %d, depthwise = %d)", path, w->M, L,
+           (int)dw);
+  cudaSetDevice(w->p->device);
+  const bool split = path == HY_MAC_TC_SPLIT || path == HY_MAC_FP64_SPLIT;
+  if (split && !w->d_R) {
+    const size_t words = (size_t)w->r_units * w->K * 2 * L * w->p->N;
+    cudaError_t ce = cudaMalloc(&w->d_R, words * sizeof(u64));
+    if (ce != cudaSuccess) {
+      w->d_R = nullptr;
+      hy_set_error("rotated-input workspace of %zu MiB: %s", words * 8 >> 20, cudaGetErrorString(ce));
+      return HY_ENOMEM;
+    }
+  }
+  w->mac_path = path;
+  return HY_OK;
+}
+
 extern "C" hy_status hy_weights_layout(const hy_weights* w, hy_layout* out) {
   HY_CHECK(w && out, HY_EINVAL, "null argument");
   *out = w->lay;
@@ -574,6 +617,7 @@ extern "C" void hy_weights_destroy(hy_weights* w) {
   cudaSetDevice(w->p->device);
   cudaFree(w->d_wt);
   cudaFree(w->d_w8);
+  cudaFree(w->d_kt);
   cudaFree(w->d_sign);
   cudaFree(w->d_D);
   cudaFree(w->d_C0);

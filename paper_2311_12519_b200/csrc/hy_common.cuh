@@ -119,8 +119,19 @@ inline int hy_mac_mpad(int M) {
   return (M + bm - 1) / bm * bm;
 }  // false if g is not odd / not in Z_2N^*
 
+// S2 + S3 kernel choice (hy_mac_path, fixed at hy_encode_weights)
+enum HyMacPath {
+  HY_MAC_THIN = 0,        // depthwise: key switching fused into a thin FP64 MAC (M <= 2 rows)
+  HY_MAC_TC_FUSED = 1,    // dense, M <= 128: key switching in the producers of the tcgen05 MAC
+  HY_MAC_TC_SPLIT = 2,    // dense, M > 128: PermAuto materialises R, tcgen05 MAC consumes it
+  HY_MAC_FP64_FUSED = 3,  // A/B option HY_MAC_FP64 (M <= 32): key switching + FP64 DFMA MAC
+  HY_MAC_FP64_SPLIT = 4,  // A/B option HY_MAC_FP64 (M > 32): PermAuto + FP64 DFMA MAC
+};
+int hy_mac_path(int M, int L, bool depthwise);
+
 struct hy_weights {
   hy_params* p;
+  int mac_path;     // HyMacPath
   hy_conv_shape shape;
   hy_layout lay;
   int M;            // MAC rows per unit
@@ -128,6 +139,8 @@ struct hy_weights {
   int wblocks;      // number of distinct weight blocks (1 dense, Jc depthwise)
   int Mpad, Kpad;   // M rounded up to the row tile, K rounded up to the MAC chunk
   double* d_wt;     // [wblocks][Kpad][Mpad] weights (exact small integers), zero padded
+  int32_t* d_kt;    // [ceil(Kpad/64)*64] K term -> (tap << 16) | input ct (-1 = padding): the fused
+                    // tensor-core MAC's term table (no integer division in its producers)
   int8_t* d_w8;     // [wblocks][Mpad/128][Kpad/32][4096]: weights as int8 in the tcgen05 K-major
                     // no-swizzle canonical layout (tensor-core MAC), zero padded
   u64* d_sign;      // [L][N] NTT form of the [k,-k] plaintext, then [L][N] Shoup companions

@@ -381,6 +381,7 @@ struct KsMacArgs {
   const double* wt;            // [wblocks][Kpad][Mpad]
   u64* out;                    // [z][M'][2][L][N], M' = M (cn 1) or M/2 (cn 2)
   const u64* sign;             // [L][N] sign plaintext (NTT), then [L][N] Shoup companions
+  const int32_t* kt;           // fused tensor-core MAC: K term -> (tap << 16) | ct (-1 = padding)
   int T, Jcb, K, Kpad, M, Mpad, wblocks, L, logN, kscale, cn;
   LimbConsts lcs;
 };
@@ -1127,15 +1128,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mac_tc_kernel(KsMacArgs a, cons
   if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS));
 }
 
-// Fused variant: the producer warps compute the key-switched R values themselves (no R in
-// HBM): per chunk of 32 terms each producer thread key-switches 4 consecutive terms of one
-// position (tap keys cached in registers, the next chunk's digit reads already in flight) and
-// byte-transposes the 4 (c0, c1) pairs into the 8 planes with PRMT.
+// Fused S2 + S3 on the tensor cores (the default for dense layers with M <= 128 MAC rows): the
+// producer warps compute the key-switched R values themselves, so R never touches HBM
+// (PAPER.md:373-378 hoisted PermAuto; :718-728 lazy MAC).  CTA = one unit, one limb, 16 positions
+// x 2 components (32 columns), one 128-row M tile; 8 warps, 2 CTAs per SM (TMEM 2 x 256 columns),
+// so one CTA's epilogue overlaps the other's main loop.  Chunk = 64 terms (two K = 32 UMMA
+// steps): every thread key-switches 4 consecutive terms of one position (tap keys held in
+// registers), byte-transposes the 4 (c0, c1) pairs into the 8 byte planes with PRMT and stores
+// one 32-bit word per plane and component.  There is no dedicated MMA warp: the LAST warp to
+// finish a chunk (shared-memory ticket) issues its 2 x 8 UMMAs (M = 128, N = 32, K = 32,
+// s8 x u8 -> s32) into the 8 TMEM accumulators, so no warp ever waits for the slowest one.  TMEM
+// is zeroed first and every UMMA accumulates: integer sums are exact, so the issue order of
+// chunks by different warps does not matter.
+constexpr int KT_THREADS = 256, KT_WARPS = KT_THREADS / 32, KT_STAGES = 3, KT_CHUNK = 64;
+constexpr int KT_STAGE_A = 2 * 4096, KT_STAGE_B = 2 * 8 * 1024;
+constexpr size_t KT_SMEM = (size_t)KT_STAGES * (KT_STAGE_A + KT_STAGE_B) + 1024;
+
 template <int LT>
-__global__ void __launch_bounds__(TC_THREADS, 1) ksmac_tc_kernel(KsMacArgs a, const int8_t* __restrict__ w8) {
-  __shared__ __align__(1024) uint8_t sA[TC_STAGES][4096];
-  __shared__ __align__(1024) uint8_t sB[TC_STAGES][8][TC_COLS * 32];
-  __shared__ __align__(8) uint64_t full_bar[TC_STAGES], empty_bar[TC_STAGES], done_bar;
+__global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, const int8_t* __restrict__ w8) {
+  extern __shared__ uint8_t kt_dyn[];
+  uint8_t* smb = reinterpret_cast<uint8_t*>(((uintptr_t)kt_dyn + 1023) & ~(uintptr_t)1023);
+  auto sA = [&](int s, int ks) { return smb + (size_t)s * (KT_STAGE_A + KT_STAGE_B) + ks * 4096; };
+  auto sB = [&](int s, int ks, int b) {
+    return smb + (size_t)s * (KT_STAGE_A + KT_STAGE_B) + KT_STAGE_A + (ks * 8 + b) * 1024;
+  };
+  __shared__ __align__(8) uint64_t empty_bar[KT_STAGES];
+  __shared__ int s_ticket[KT_STAGES];
   __shared__ uint32_t s_tmem;
   __shared__ const u64* s_key[HY_MAX_TAPS];
   __shared__ GaloisAct s_act[HY_MAX_TAPS];
@@ -1146,22 +1164,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) ksmac_tc_kernel(KsMacArgs a, co
   const int l = blockIdx.x / tiles, j0 = (blockIdx.x % tiles) * TC_POS;
   const int mt = blockIdx.y, z = blockIdx.z;
   const int nmt = (a.Mpad + 127) / 128;
-  const int nchunks = a.Kpad / 32;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int nk32 = a.Kpad / 32;
+  const int nchunks = (nk32 + 1) / 2;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  for (int t = tid; t < a.T; t += TC_THREADS) {
+  for (int t = tid; t < a.T; t += KT_THREADS) {
     s_key[t] = a.keys[t];
     s_act[t] = a.act[t];
   }
+  if (tid < KT_STAGES) s_ticket[tid] = 0;
   if (tid == 0) {
-    for (int s = 0; s < TC_STAGES; s++) {
-      mbar_init(&full_bar[s], 128);
-      mbar_init(&empty_bar[s], 1);
-    }
-    mbar_init(&done_bar, 1);
+    for (int s = 0; s < KT_STAGES; s++) mbar_init(&empty_bar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 4) {
+  if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
                  "r"(TC_TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -1170,118 +1186,169 @@ __global__ void __launch_bounds__(TC_THREADS, 1) ksmac_tc_kernel(KsMacArgs a, co
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
+  const int quad = warp & 3, chalf = warp >> 2;  // TMEM lanes 32 quad .. and columns half chalf
+  {
+    const uint32_t zb = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(chalf * TC_TMEM_COLS / 2);
+    const uint32_t z0 = 0;
+#pragma unroll 1
+    for (int c = 0; c < (int)TC_TMEM_COLS / 2; c += 8)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(zb + c), "r"(z0)
+                   : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
 
-  if (tid < 128) {
-    // ---------------- producers ----------------
-    const int pos = tid & 15, kg = tid >> 4;  // position, terms 4kg .. 4kg+3 of each chunk
-    const int j = j0 + pos;
-    const LimbConst cst = a.lcs.lc[l];
-    const int8_t* wsrc = w8 + ((size_t)(z % a.wblocks) * nmt + mt) * nchunks * 4096;
-    const u64* C0u = a.C0 + (size_t)z * a.Jcb * LN + (size_t)l * N;
-    const u64* Du = a.D + (size_t)z * a.Jcb * LT * LN + (size_t)l * N;
-    // plane byte offsets (K-major canonical) of column pos (c0) and 16 + pos (c1), terms 4kg..4kg+3
-    const int off0 = (pos >> 3) * 256 + (kg >> 2) * 128 + (pos & 7) * 16 + (kg & 3) * 4;
-    const int off1 = off0 + 2 * 256;
-    KeyRegs<LT> kr;
-    RPre<LT> pre[4];
-    auto load_chunk = [&](int ch, RPre<LT>* pr) {
+  // ---------------- producers (all warps) ----------------
+  const int pos = tid & 15, tg = tid >> 4;  // position; terms 4 tg .. 4 tg + 3 of each chunk
+  const int ks = tg >> 3, kg = tg & 7;
+  const int j = j0 + pos;
+  const u64 q = a.lcs.lc[l].q;
+  const int8_t* wsrc = w8 + ((size_t)(z % a.wblocks) * nmt + mt) * nk32 * 4096;
+  const u64* C0u = a.C0 + (size_t)z * a.Jcb * LN + (size_t)l * N;
+  const u64* Du = a.D + (size_t)z * a.Jcb * LT * LN + (size_t)l * N;
+  // K-major canonical plane offsets of column pos (c0) and 16 + pos (c1), terms 4kg .. 4kg + 3
+  const int off0 = (pos >> 3) * 256 + (kg >> 2) * 128 + (pos & 7) * 16 + (kg & 3) * 4;
+  const int off1 = off0 + 2 * 256;
+  // the tap's key words for (limb l, position j): digit i, component b/a, then Shoup companions
+  int ktap = -1;
+  u64 kv[2 * LT], ksh[2 * LT];
+  struct Term {
+    u64 c0, d[LT];
+    int tap;  // -1 = padding term (R = 0)
+  } pre[4];
+  auto load_chunk = [&](int ch) {
 #pragma unroll
-      for (int t = 0; t < 4; t++) {
-        const int kk = ch * 32 + kg * 4 + t;
-        pr[t].t = -1;
-        if (kk >= a.K) continue;
-        const int tap = kk / a.Jcb, c = kk - tap * a.Jcb;
-        pr[t].t = tap;
-        const u64* C0 = C0u + (size_t)c * LN;
-        const u64* D = Du + (size_t)c * LT * LN;
-        if (s_key[tap] == nullptr) {
-          pr[t].c0 = __ldg(C0 + j);
-          pr[t].d[0] = __ldg(D + (size_t)l * LN + j);
+    for (int t = 0; t < 4; t++) {
+      const int e = __ldg(a.kt + ch * KT_CHUNK + tg * 4 + t);
+      pre[t].tap = e < 0 ? -1 : e >> 16;
+      if (e < 0) continue;
+      const int tap = e >> 16, c = e & 0xffff;
+      const u64* C0 = C0u + (size_t)c * LN;
+      const u64* D = Du + (size_t)c * LT * LN;
+      if (s_key[tap] == nullptr) {  // identity tap: R = (C0_c, D_{c,l}) in limb l
+        pre[t].c0 = __ldg(C0 + j);
+        pre[t].d[0] = __ldg(D + (size_t)l * LN + j);
+      } else {
+        const int jp = galois_perm(j, s_act[tap], N >> 1);
+        pre[t].c0 = __ldg(C0 + jp);
+#pragma unroll
+        for (int i = 0; i < LT; i++) pre[t].d[i] = __ldg(D + (size_t)i * LN + jp);
+      }
+    }
+  };
+  const uint32_t idesc = umma_idesc_s8u8(128, TC_COLS);
+  // one register buffer: the next chunk's digit reads are issued right after this chunk's key
+  // switching (their latency is covered by the other resident warps: 2 CTAs x 8 warps per SM)
+  load_chunk(0);
+  for (int ch = 0; ch < nchunks; ch++) {
+    const int s = ch % KT_STAGES;
+    const bool has_ks = 2 * ch + ks < nk32;
+    // weights: K step ws = tid >> 7 of this chunk, 2 x 16 B per thread
+    const int ws = tid >> 7;
+    const bool has_w = 2 * ch + ws < nk32;
+    uint4 wv = make_uint4(0, 0, 0, 0), wv2 = make_uint4(0, 0, 0, 0);
+    if (has_w) {
+      const uint4* wp = reinterpret_cast<const uint4*>(wsrc + (size_t)(2 * ch + ws) * 4096) + (tid & 127);
+      wv = __ldg(wp);
+      wv2 = __ldg(wp + 128);
+    }
+    // key switching, fully lazy: Shoup products are in [0, 2q), so R.c0 < (2L + 1) q and
+    // R.c1 < 2L q stay below 2^64 (q < 2^60, L <= 5 -> 11 q).  The MAC is exact for any 64-bit
+    // R (byte planes), and the epilogue's single reduction makes the output canonical, so R
+    // needs no reduction at all.
+    uint32_t lo0[4], hi0[4], lo1[4], hi1[4];
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      const int tap = pre[t].tap;
+      u64 r0 = 0, r1 = 0;
+      if (tap >= 0) {
+        const u64* key = s_key[tap];
+        if (key == nullptr) {
+          r0 = pre[t].c0;
+          r1 = pre[t].d[0];
         } else {
-          const int jp = galois_perm(j, s_act[tap], N >> 1);
-          pr[t].c0 = __ldg(C0 + jp);
+          if (tap != ktap) {
+            const u64* kb = key + (size_t)l * N + j;
+            const size_t kblk = 2 * LT * LN;
 #pragma unroll
-          for (int i = 0; i < LT; i++) pr[t].d[i] = __ldg(D + (size_t)i * LN + jp);
+            for (int x = 0; x < 2 * LT; x++) {
+              kv[x] = __ldg(kb + x * LN);
+              ksh[x] = __ldg(kb + x * LN + kblk);
+            }
+            ktap = tap;
+          }
+          r0 = pre[t].c0;
+#pragma unroll
+          for (int i = 0; i < LT; i++) {
+            r0 += shoup_mul(pre[t].d[i], kv[2 * i], ksh[2 * i], q);
+            r1 += shoup_mul(pre[t].d[i], kv[2 * i + 1], ksh[2 * i + 1], q);
+          }
         }
       }
-    };
-    load_chunk(0, pre);
-    for (int ch = 0; ch < nchunks; ch++) {
-      const int s = ch % TC_STAGES;
-      RPre<LT> cur[4];
-#pragma unroll
-      for (int t = 0; t < 4; t++) cur[t] = pre[t];
-      if (ch + 1 < nchunks) load_chunk(ch + 1, pre);
-      const uint4 wa = __ldg(reinterpret_cast<const uint4*>(wsrc + (size_t)ch * 4096) + tid);
-      const uint4 wb = __ldg(reinterpret_cast<const uint4*>(wsrc + (size_t)ch * 4096) + 128 + tid);
-      uint32_t lo0[4], hi0[4], lo1[4], hi1[4];
-#pragma unroll
-      for (int t = 0; t < 4; t++) {
-        u64 r0, r1;
-        r_finish<LT>(a, s_key, cur[t], l, j, cst, kr, r0, r1);
-        lo0[t] = (uint32_t)r0;
-        hi0[t] = (uint32_t)(r0 >> 32);
-        lo1[t] = (uint32_t)r1;
-        hi1[t] = (uint32_t)(r1 >> 32);
-      }
-      // 4x4 byte transposes: word b of plane b holds byte b of the 4 terms
-      auto tr4 = [](const uint32_t* x, uint32_t* w) {
-        const uint32_t t0 = __byte_perm(x[0], x[1], 0x5140), t1 = __byte_perm(x[0], x[1], 0x7362);
-        const uint32_t t2 = __byte_perm(x[2], x[3], 0x5140), t3 = __byte_perm(x[2], x[3], 0x7362);
-        w[0] = __byte_perm(t0, t2, 0x5410);
-        w[1] = __byte_perm(t0, t2, 0x7632);
-        w[2] = __byte_perm(t1, t3, 0x5410);
-        w[3] = __byte_perm(t1, t3, 0x7632);
-      };
-      uint32_t p0[8], p1[8];
-      tr4(lo0, p0);
-      tr4(hi0, p0 + 4);
-      tr4(lo1, p1);
-      tr4(hi1, p1 + 4);
-      if (ch >= TC_STAGES) mbar_wait(&empty_bar[s], ((ch / TC_STAGES) - 1) & 1);
-      reinterpret_cast<uint4*>(sA[s])[tid] = wa;
-      reinterpret_cast<uint4*>(sA[s])[128 + tid] = wb;
+      lo0[t] = (uint32_t)r0;
+      hi0[t] = (uint32_t)(r0 >> 32);
+      lo1[t] = (uint32_t)r1;
+      hi1[t] = (uint32_t)(r1 >> 32);
+    }
+    if (ch + 1 < nchunks) load_chunk(ch + 1);
+    uint32_t p0[8], p1[8];
+    byte_tr4(lo0, p0);
+    byte_tr4(hi0, p0 + 4);
+    byte_tr4(lo1, p1);
+    byte_tr4(hi1, p1 + 4);
+    if (ch >= KT_STAGES) mbar_wait(&empty_bar[s], ((ch / KT_STAGES) - 1) & 1);
+    if (has_w) {
+      reinterpret_cast<uint4*>(sA(s, ws))[tid & 127] = wv;
+      reinterpret_cast<uint4*>(sA(s, ws))[128 + (tid & 127)] = wv2;
+    }
+    if (has_ks) {
 #pragma unroll
       for (int b = 0; b < 8; b++) {
-        *reinterpret_cast<uint32_t*>(&sB[s][b][off0]) = p0[b];
-        *reinterpret_cast<uint32_t*>(&sB[s][b][off1]) = p1[b];
+        *reinterpret_cast<uint32_t*>(sB(s, ks, b) + off0) = p0[b];
+        *reinterpret_cast<uint32_t*>(sB(s, ks, b) + off1) = p1[b];
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&full_bar[s]);
     }
-  } else if (tid == 128) {
-    const uint32_t idesc = umma_idesc_s8u8(128, TC_COLS);
-    for (int ch = 0; ch < nchunks; ch++) {
-      const int s = ch % TC_STAGES;
-      mbar_wait(&full_bar[s], (ch / TC_STAGES) & 1);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint64_t da = umma_desc_kmajor(smem_u32(sA[s]));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      const int prev = atomicAdd(&s_ticket[s], 1);  // monotonic: use u of stage s takes tickets
+      if (prev % KT_WARPS == KT_WARPS - 1) {       // 8u .. 8u + 7; the last warp issues the UMMAs
+        __threadfence_block();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        for (int k2 = 0; k2 < 2 && 2 * ch + k2 < nk32; k2++) {
+          const uint64_t da = umma_desc_kmajor(smem_u32(sA(s, k2)));
 #pragma unroll
-      for (int b = 0; b < 8; b++) {
-        const uint64_t db = umma_desc_kmajor(smem_u32(sB[s][b]));
-        const uint32_t acc = ch > 0;
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (uint32_t)(b * TC_COLS)),
-            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          for (int b = 0; b < 8; b++) {
+            const uint64_t db = umma_desc_kmajor(smem_u32(sB(s, k2, b)));
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (uint32_t)(b * TC_COLS)),
+                "l"(da), "l"(db), "r"(idesc));
+          }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(&empty_bar[s]))
+                     : "memory");
       }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       smem_u32(&empty_bar[s]))
-                   : "memory");
     }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     smem_u32(&done_bar))
-                 : "memory");
+    __syncwarp();
   }
 
-  if (tid < 128) {
-    mbar_wait(&done_bar, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int row = mt * 128 + warp * 32 + (tid & 31);
-    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+  // ---------------- epilogue: warp w reads TMEM lanes 32 (w % 4) .., columns of component w / 4
+  // every chunk's UMMAs are complete once the last KT_STAGES chunks' commits have arrived (earlier
+  // stages were waited for before their reuse)
+  for (int ch = nchunks > KT_STAGES ? nchunks - KT_STAGES : 0; ch < nchunks; ch++)
+    mbar_wait(&empty_bar[ch % KT_STAGES], (ch / KT_STAGES) & 1);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  {
+    const int comp = chalf;
+    const int row = mt * 128 + quad * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
-    for (int c0 = 0; c0 < TC_COLS; c0 += 8) {
-      uint32_t v[8][8];
+    for (int c0 = comp * 16; c0 < comp * 16 + 16; c0 += 8) {
+      uint32_t v[8][8];  // [plane][column]
 #pragma unroll
       for (int b = 0; b < 8; b++) {
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -1304,14 +1371,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) ksmac_tc_kernel(KsMacArgs a, co
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS));
 }
 
 template <int LT>
 hy_status launch_ksmac_tc(const KsMacArgs& a, const int8_t* w8, int units, cudaStream_t s) {
   const int N = 1 << a.logN;
+  static bool attr_done = false;
+  if (!attr_done) {
+    HY_CUDA_TRY(cudaFuncSetAttribute(ksmac_tc_kernel<LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)KT_SMEM));
+    attr_done = true;
+  }
   dim3 grid((unsigned)(a.L * (N / TC_POS)), (unsigned)((a.Mpad + 127) / 128), (unsigned)units);
-  ksmac_tc_kernel<LT><<<grid, TC_THREADS, 0, s>>>(a, w8);
+  ksmac_tc_kernel<LT><<<grid, KT_THREADS, KT_SMEM, s>>>(a, w8);
   HY_LAUNCH_CHECK();
   return HY_OK;
 }
@@ -1456,6 +1528,7 @@ hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
   a.wt = w->d_wt;
   a.out = w->d_P;
   a.sign = w->d_sign;
+  a.kt = w->d_kt;
   a.T = (int)lay.n_taps;
   a.Jcb = dw ? 1 : (int)lay.Jc;
   a.K = w->K;
@@ -1470,11 +1543,8 @@ hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
   a.lcs = limb_consts(p);
   const int units = (int)(dw ? nunits * lay.Jc : nunits);
   const int tile = hy_mac_tile(w->M);
-  static const bool fused = getenv("HY_FUSED_KSMAC") != nullptr;  // A/B switches
-  static const bool fp64_mac = getenv("HY_MAC_FP64") != nullptr;
-  // depthwise, or M <= 32 MAC rows (C1, C2: latency-bound small layers): key switching fused into
-  // the FP64 MAC; dense M >= 64: PermAuto + tensor-core MAC
-  if (dw || tile < 8 || fused) {
+  const int path = w->mac_path;
+  if (path == HY_MAC_THIN || path == HY_MAC_FP64_FUSED) {  // key switching fused into the FP64 MAC
     HY_TRY(mac_mark(w, s));
     if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[0], s));
     hy_status st;
@@ -1488,8 +1558,7 @@ hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
     w->mac_launches = 1;
     return HY_OK;
   }
-  static const bool fused_tc = getenv("HY_FUSED_TC") != nullptr && !fp64_mac;  // experimental (slower)
-  if (fused_tc && (p->L == 2 || p->L == 3 || p->L == 5)) {  // fused key switching + tensor-core MAC
+  if (path == HY_MAC_TC_FUSED) {  // key switching in the producers of the tensor-core MAC
     HY_TRY(mac_mark(w, s));
     if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[0], s));
     hy_status st = p->L == 2 ? launch_ksmac_tc<2>(a, w->d_w8, units, s)
@@ -1500,6 +1569,7 @@ hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
     w->mac_launches = 1;
     return HY_OK;
   }
+  const bool fp64_mac = path == HY_MAC_FP64_SPLIT;
   // dense: PermAuto materialises R for a batch of units, the MAC GEMM consumes it
   const size_t LN = (size_t)p->L * p->N;
   const int mrows = lay.cn == 2 ? w->M / 2 : w->M;  // output ciphertexts per unit
@@ -1604,3 +1674,12 @@ hy_status decrypt_phase(const hy_params* p, const u64* s_ntt, const u64* s_ntt_s
 }
 
 }  // namespace hyk
+
+int hy_mac_path(int M, int L, bool depthwise) {
+  if (depthwise) return HY_MAC_THIN;
+  static const bool fp64 = getenv("HY_MAC_FP64") != nullptr;    // A/B switches
+  static const bool split = getenv("HY_SPLIT_TC") != nullptr;
+  if (fp64) return M <= 32 ? HY_MAC_FP64_FUSED : HY_MAC_FP64_SPLIT;
+  if (!split && M <= 128 && (L == 2 || L == 3 || L == 5)) return HY_MAC_TC_FUSED;
+  return HY_MAC_TC_SPLIT;
+}

@@ -16,7 +16,8 @@ __all__ = ["HyenaError", "hy_conv_shape", "hy_layout", "load_library", "library_
            "hy_plan_layout", "hy_params_create", "hy_params_destroy", "hy_keys_upload", "hy_encode_weights",
            "hy_weights_layout", "hy_weights_destroy", "hy_conv_eval", "hy_conv_eval_host", "hy_poly_mul",
            "hy_ntt_roundtrip", "hy_rotate", "hy_decrypt_debug", "hy_kernel_launches", "hy_weights_set_stage_events",
-           "hy_weights_mac_time", "layout_dict", "EXPORTED"]
+           "hy_weights_mac_time", "hy_weights_mac_path", "hy_weights_set_mac_path", "MAC_PATHS", "layout_dict",
+           "EXPORTED"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 HY_MAX_TAPS = 49
@@ -26,7 +27,10 @@ HY_MAX_GALOIS = 64
 EXPORTED = ["hy_last_error", "hy_plan_layout", "hy_params_create", "hy_params_destroy", "hy_keys_upload",
             "hy_encode_weights", "hy_weights_layout", "hy_weights_destroy", "hy_conv_eval", "hy_conv_eval_host",
             "hy_poly_mul", "hy_ntt_roundtrip", "hy_rotate", "hy_decrypt_debug", "hy_kernel_launches",
-            "hy_weights_set_stage_events", "hy_weights_mac_time"]
+            "hy_weights_set_stage_events", "hy_weights_mac_time", "hy_weights_mac_path", "hy_weights_set_mac_path"]
+
+# S2 + S3 kernel choices (include/hyena.h hy_weights_mac_path)
+MAC_PATHS = {"thin": 0, "tc_fused": 1, "tc_split": 2, "fp64_fused": 3, "fp64_split": 4}
 
 
 class HyenaError(RuntimeError):
@@ -90,6 +94,8 @@ def load_library() -> ctypes.CDLL:
         "hy_kernel_launches": (u64, []),
         "hy_weights_set_stage_events": (i32, [vp, vp, u32]),
         "hy_weights_mac_time": (i32, [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(u32)]),
+        "hy_weights_mac_path": (i32, [vp, ctypes.POINTER(i32)]),
+        "hy_weights_set_mac_path": (i32, [vp, i32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -238,3 +244,14 @@ def hy_weights_mac_time(w: int):
     ms, n = ctypes.c_float(), ctypes.c_uint32()
     _check(load_library().hy_weights_mac_time(w, ctypes.byref(ms), ctypes.byref(n)), "hy_weights_mac_time")
     return float(ms.value), int(n.value)
+
+
+def hy_weights_mac_path(w: int) -> str:
+    """Name of the S2 + S3 kernel path hy_conv_eval uses for these weights (MAC_PATHS)."""
+    v = ctypes.c_int32()
+    _check(load_library().hy_weights_mac_path(w, ctypes.byref(v)), "hy_weights_mac_path")
+    return {i: n for n, i in MAC_PATHS.items()}[v.value]
+
+
+def hy_weights_set_mac_path(w: int, path: str) -> None:
+    _check(load_library().hy_weights_set_mac_path(w, MAC_PATHS[path]), "hy_weights_set_mac_path")

@@ -22,7 +22,7 @@ def hy():
     return pkg
 
 
-def run_gpu(hy, lay, shape_kw, units=None):
+def run_gpu(hy, lay, shape_kw, units=None, path=None):
     p = hy.hy_params_create(lay.P.N, lay.P.primes, lay.P.t, 0)
     try:
         elts = list(lay.keys)
@@ -30,6 +30,13 @@ def run_gpu(hy, lay, shape_kw, units=None):
             hy.hy_keys_upload(p, elts, np.stack([lay.keys[g] for g in elts]))
         w = hy.hy_encode_weights(p, lay.W, **shape_kw)
         try:
+            if path is not None:
+                try:
+                    hy.hy_weights_set_mac_path(w, path)
+                except hy.HyenaError as e:
+                    assert "not valid" in str(e)
+                    pytest.skip(f"MAC path {path} does not apply to this layout")
+                assert hy.hy_weights_mac_path(w) == path
             L = hy.hy_weights_layout(w)
             assert (L.J, L.Jout, L.cn, L.k) == (lay.plan.J, lay.plan.Jout, lay.plan.cn, lay.ls.k)
             nu = L.U if units is None else units
@@ -79,7 +86,7 @@ CASES = {
     "k5x5": dict(N=2048, bits=50, L=2, batch=1, Ci=2, Co=2, H=8, W=8, kh=5, kw=5, pad=2),
     "wide_weights": dict(N=2048, bits=60, L=3, batch=1, Ci=8, Co=8, H=6, W=6, kh=3, kw=3, pad=1,
                          xrange=(-128, 128), wrange=(-128, 128)),
-    # >= 64 MAC rows: the tensor-core MAC path (tcgen05 kind::i8), with row padding to 128
+    # 64 .. 140 MAC rows (row padding to 128, two M tiles above 128), L = 2/3/5
     "tc_cn2_rows140": dict(N=1024, bits=50, L=2, batch=5, Ci=3, Co=70, H=6, W=6, kh=3, kw=3, pad=1,
                            xrange=(-128, 128), wrange=(-128, 128)),
     "tc_cn1_units": dict(N=1024, bits=50, L=3, batch=17, Ci=3, Co=70, H=6, W=6, kh=3, kw=3, pad=1,
@@ -88,15 +95,23 @@ CASES = {
                    xrange=(-128, 128), wrange=(-128, 128)),
     "tc_cn2_L5_rows130": dict(N=1024, bits=50, L=5, batch=2, Ci=2, Co=65, H=5, W=5, kh=3, kw=3, pad=1),
     "tc_pw_cn1": dict(N=1024, bits=50, L=3, batch=9, Ci=40, Co=66, H=6, W=6, kh=1, kw=1, pad=0),
+    # K = Jc * 9 = 297 terms: 5 chunks of 64 with a ragged last K step; 128 rows exactly
+    "tc_cn2_k297_rows128": dict(N=1024, bits=60, L=3, batch=1, Ci=66, Co=64, H=5, W=5, kh=3, kw=3, pad=1,
+                                xrange=(-128, 128), wrange=(-128, 128)),
 }
 
 
+PATHS = ["default", "tc_fused", "tc_split", "fp64_fused", "fp64_split", "thin"]
+
+
+@pytest.mark.parametrize("path", PATHS)
 @pytest.mark.parametrize("name", sorted(CASES))
-def test_conv_bit_exact_small(hy, name):
+def test_conv_bit_exact_small(hy, name, path):
+    """Every S2+S3 kernel path that applies to the layout gives the oracle's bits."""
     c = dict(CASES[name])
     N, bits, L = c.pop("N"), c.pop("bits"), c.pop("L")
     lay = make_layer(N, ntt_primes(N, bits, L), seed=500 + sorted(CASES).index(name), **c)
-    got, dec, Lay = run_gpu(hy, lay, shape_of(lay))
+    got, dec, Lay = run_gpu(hy, lay, shape_of(lay), path=None if path == "default" else path)
     ref = conv.he_conv(lay.P, lay.ls, lay.W, lay.ct_in, lay.keys)
     for i in range(Lay.Jout):
         assert np.array_equal(got[i], ref[i]), f"output ct {i} differs"

@@ -5,11 +5,16 @@ for f in sorted(glob.glob('gpurun_out/bench_*.log')):
     for l in open(f):
         if l.startswith('{'):
             d = json.loads(l)
+            if 'roofline' not in d:
+                print(f"{f[16:-4]:12s} reference {d['value']:.4g} {d['unit']}")
+                continue
             r = d['roofline']
-            print(f"{f[16:-4]:12s} {d['value']:10.2f} {d['unit']} ms={d['ms_per_step']:.3f} "
-                  f"stages={ {k: round(v, 3) for k, v in d['stages_ms'].items()} } "
-                  f"roof={r.get('kernel')}:{r['frac']:.3f} of {r['peak']:.1f} {r['unit']} clk={d['clocks']['sm_mhz']} "
+            print(f"{f[16:-4]:12s} {d['value']:10.2f} {d['unit']} ms={d['ms_per_step']:.3f} path={d.get('mac_path')} "
+                  f"stages={ {k: round(v, 3) for k, v in d['stages_ms'].items()} } clk={d['clocks']['sm_mhz']} "
                   f"e2e={d['e2e']['value']:.2f}")
+            for k, v in r.get('stages', {}).items():
+                print(f"      {k:18s} {v['bound']} {v['achieved']:.1f}/{v['peak']:.1f} {v['unit']} frac={v['frac']:.3f}"
+                      + (f" tc={v['tensor_int8']['frac']:.3f}" if 'tensor_int8' in v else ''))
 for f in sorted(glob.glob('gpurun_out/launches*.csv')):
     rows = [r for r in csv.reader(open(f)) if len(r) > 5]
     hdr, rows = rows[0], rows[1:]

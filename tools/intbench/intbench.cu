@@ -89,6 +89,25 @@ __global__ void k_iadd3(const int32_t* __restrict__ w, int64_t* out, int n) {
   if (s == 0x12345) out[0] = s;
 }
 
+// 64-bit Shoup modular product x * w mod q (in [0, 2q)), the unit of every "alu" roofline in
+// bench.py: 8 independent chains per thread
+__global__ void k_shoup(const int32_t* __restrict__ w, int64_t* out, int n) {
+  const uint64_t q = 0xfffffffffffc001ull;
+  const uint64_t wv = 0x0123456789abcdeull + (uint64_t)w[threadIdx.x & 31];
+  const uint64_t wsh = (uint64_t)(((unsigned __int128)wv << 64) / q);
+  uint64_t acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) acc[i] = (uint64_t)w[(threadIdx.x + i) & 31] * 0x9E3779B97F4A7C15ull;
+  for (int it = 0; it < ITERS; it++) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) acc[i] = acc[i] * wv - __umul64hi(acc[i], wsh) * q;
+  }
+  uint64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) s += acc[i];
+  if (s == 0x123456789) out[0] = s;
+}
+
 typedef void (*kfn)(const int32_t*, int64_t*, int);
 
 static void run(const char* name, kfn f, double ops_per_inner, int* w, int64_t* o) {
@@ -122,6 +141,7 @@ int main() {
   run("imad_s32", k_imad32, 1, w, o);
   run("umul64hi", k_mulhi64, 1, w, o);
   run("dfma", k_dfma, 1, w, o);
+  run("shoup_modmul64", k_shoup, 1, w, o);
   run("iadd_xor_shift(3 ops)", k_iadd3, 3, w, o);
   cudaError_t e = cudaDeviceSynchronize();
   printf("status %s\n", cudaGetErrorString(e));

@@ -1070,19 +1070,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mac_tc_kernel(KsMacArgs a, cons
     }
   } else if (tid == 128) {
     // ---------------- MMA issuer ----------------
-    const uint32_t idesc = umma_idesc_s8u8(128, TC_COLS);
+    // the 8 byte planes are consecutive 8-column core-matrix groups of ONE B operand (SBO = 256 B
+    // throughout), so a single UMMA with N = 8 x 32 = 256 covers all planes: D column = 32 b + col
+    const uint32_t idesc = umma_idesc_s8u8(128, 8 * TC_COLS);
     for (int ch = 0; ch < nchunks; ch++) {
       const int s = ch % TC_STAGES;
       mbar_wait(&full_bar[s], (ch / TC_STAGES) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint64_t da = umma_desc_kmajor(smem_u32(sA[s]));
-#pragma unroll
-      for (int b = 0; b < 8; b++) {
-        const uint64_t db = umma_desc_kmajor(smem_u32(sB[s][b]));
+      {
+        const uint64_t db = umma_desc_kmajor(smem_u32(sB[s][0]));
         const uint32_t acc = ch > 0;
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (uint32_t)(b * TC_COLS)),
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
             "l"(da), "l"(db), "r"(idesc), "r"(acc));
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -1132,17 +1133,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mac_tc_kernel(KsMacArgs a, cons
 // producer warps compute the key-switched R values themselves, so R never touches HBM
 // (PAPER.md:373-378 hoisted PermAuto; :718-728 lazy MAC).  CTA = one unit, one limb, 16 positions
 // x 2 components (32 columns), one 128-row M tile; 8 warps, 2 CTAs per SM (TMEM 2 x 256 columns),
-// so one CTA's epilogue overlaps the other's main loop.  Chunk = 64 terms (two K = 32 UMMA
-// steps): every thread key-switches 4 consecutive terms of one position (tap keys held in
-// registers), byte-transposes the 4 (c0, c1) pairs into the 8 byte planes with PRMT and stores
-// one 32-bit word per plane and component.  There is no dedicated MMA warp: the LAST warp to
-// finish a chunk (shared-memory ticket) issues its 2 x 8 UMMAs (M = 128, N = 32, K = 32,
-// s8 x u8 -> s32) into the 8 TMEM accumulators, so no warp ever waits for the slowest one.  TMEM
-// is zeroed first and every UMMA accumulates: integer sums are exact, so the issue order of
-// chunks by different warps does not matter.
-constexpr int KT_THREADS = 256, KT_WARPS = KT_THREADS / 32, KT_STAGES = 3, KT_CHUNK = 64;
-constexpr int KT_STAGE_A = 2 * 4096, KT_STAGE_B = 2 * 8 * 1024;
-constexpr size_t KT_SMEM = (size_t)KT_STAGES * (KT_STAGE_A + KT_STAGE_B) + 1024;
+// so one CTA's epilogue overlaps the other's main loop.  The CTA's key words (every tap, 16
+// positions, limb l) are staged in shared memory once.  Chunk = 64 terms (two K = 32 UMMA steps):
+// every thread key-switches 4 consecutive terms of one position, byte-transposes the 4 (c0, c1)
+// pairs into the 8 byte planes with PRMT and stores one 32-bit word per plane and component; the
+// digit reads of chunk ch + 1 are in flight while chunk ch is switched (register double buffer).
+// There is no dedicated MMA warp: the LAST warp to finish a chunk (shared-memory ticket) issues
+// its 2 x 8 UMMAs (M = 128, N = 32, K = 32, s8 x u8 -> s32) into the 8 TMEM accumulators.  TMEM is
+// zeroed first and every UMMA accumulates: integer sums are exact, so the issue order of chunks by
+// different warps does not matter.
+constexpr int KT_THREADS = 384, KT_WARPS = KT_THREADS / 32, KT_STAGES = 2, KT_KS = 3, KT_CHUNK = 32 * KT_KS;
+constexpr int KT_STAGE_A = KT_KS * 4096, KT_STAGE_B = KT_KS * 8 * 1024;
+constexpr size_t KT_SMEM_MMA = (size_t)KT_STAGES * (KT_STAGE_A + KT_STAGE_B) + 1024;
+inline size_t kt_smem(int T, int L) { return KT_SMEM_MMA + (size_t)T * 4 * L * TC_POS * sizeof(u64); }
 
 template <int LT>
 __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, const int8_t* __restrict__ w8) {
@@ -1152,10 +1155,12 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   auto sB = [&](int s, int ks, int b) {
     return smb + (size_t)s * (KT_STAGE_A + KT_STAGE_B) + KT_STAGE_A + (ks * 8 + b) * 1024;
   };
+  // keys: [tap][x = 2 digit + comp][2: value, Shoup][16 positions]
+  u64* skey = reinterpret_cast<u64*>(smb + (size_t)KT_STAGES * (KT_STAGE_A + KT_STAGE_B));
   __shared__ __align__(8) uint64_t empty_bar[KT_STAGES];
   __shared__ int s_ticket[KT_STAGES];
   __shared__ uint32_t s_tmem;
-  __shared__ const u64* s_key[HY_MAX_TAPS];
+  __shared__ int s_haskey[HY_MAX_TAPS];
   __shared__ GaloisAct s_act[HY_MAX_TAPS];
 
   const int N = 1 << a.logN;
@@ -1165,12 +1170,19 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   const int mt = blockIdx.y, z = blockIdx.z;
   const int nmt = (a.Mpad + 127) / 128;
   const int nk32 = a.Kpad / 32;
-  const int nchunks = (nk32 + 1) / 2;
+  const int nchunks = (nk32 + KT_KS - 1) / KT_KS;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   for (int t = tid; t < a.T; t += KT_THREADS) {
-    s_key[t] = a.keys[t];
+    s_haskey[t] = a.keys[t] != nullptr;
     s_act[t] = a.act[t];
+  }
+  // stage the key words of this CTA (limb l, positions j0 .. j0 + 15) for every tap
+  for (int e = tid; e < a.T * 4 * LT * TC_POS; e += KT_THREADS) {
+    const int p = e % TC_POS, r = e / TC_POS;
+    const int sh = r % 2, x = (r / 2) % (2 * LT), tap = r / (4 * LT);
+    const u64* key = a.keys[tap];
+    skey[e] = key ? __ldg(key + (size_t)sh * 2 * LT * LN + (size_t)x * LN + (size_t)l * N + j0 + p) : 0ull;
   }
   if (tid < KT_STAGES) s_ticket[tid] = 0;
   if (tid == 0) {
@@ -1187,7 +1199,7 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
   const int quad = warp & 3, chalf = warp >> 2;  // TMEM lanes 32 quad .. and columns half chalf
-  {
+  if (warp < 8) {
     const uint32_t zb = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(chalf * TC_TMEM_COLS / 2);
     const uint32_t z0 = 0;
 #pragma unroll 1
@@ -1210,46 +1222,51 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   // K-major canonical plane offsets of column pos (c0) and 16 + pos (c1), terms 4kg .. 4kg + 3
   const int off0 = (pos >> 3) * 256 + (kg >> 2) * 128 + (pos & 7) * 16 + (kg & 3) * 4;
   const int off1 = off0 + 2 * 256;
-  // the tap's key words for (limb l, position j): digit i, component b/a, then Shoup companions
-  int ktap = -1;
-  u64 kv[2 * LT], ksh[2 * LT];
+  const float inv_jc = 1.0f / (float)a.Jcb;
   struct Term {
     u64 c0, d[LT];
-    int tap;  // -1 = padding term (R = 0)
-  } pre[4];
-  auto load_chunk = [&](int ch) {
+    int tap;  // -1 = padding term (R = 0); identity tap: d[0] = D_{c,l}
+  };
+  Term pre[4];
+  auto load_chunk = [&](int ch, Term* pr) {
 #pragma unroll
     for (int t = 0; t < 4; t++) {
-      const int e = __ldg(a.kt + ch * KT_CHUNK + tg * 4 + t);
-      pre[t].tap = e < 0 ? -1 : e >> 16;
-      if (e < 0) continue;
-      const int tap = e >> 16, c = e & 0xffff;
+      const int kk = ch * KT_CHUNK + tg * 4 + t;
+      pr[t].tap = -1;
+      if (kk >= a.K) continue;
+      int tap = (int)((float)kk * inv_jc);  // kk / Jcb (kk < 2^16: off by at most one)
+      if (tap * a.Jcb > kk) tap--;
+      if ((tap + 1) * a.Jcb <= kk) tap++;
+      const int c = kk - tap * a.Jcb;
+      pr[t].tap = tap;
       const u64* C0 = C0u + (size_t)c * LN;
       const u64* D = Du + (size_t)c * LT * LN;
-      if (s_key[tap] == nullptr) {  // identity tap: R = (C0_c, D_{c,l}) in limb l
-        pre[t].c0 = __ldg(C0 + j);
-        pre[t].d[0] = __ldg(D + (size_t)l * LN + j);
+      if (!s_haskey[tap]) {  // identity tap: R = (C0_c, D_{c,l}) in limb l
+        pr[t].c0 = __ldg(C0 + j);
+        pr[t].d[0] = __ldg(D + (size_t)l * LN + j);
       } else {
         const int jp = galois_perm(j, s_act[tap], N >> 1);
-        pre[t].c0 = __ldg(C0 + jp);
+        pr[t].c0 = __ldg(C0 + jp);
 #pragma unroll
-        for (int i = 0; i < LT; i++) pre[t].d[i] = __ldg(D + (size_t)i * LN + jp);
+        for (int i = 0; i < LT; i++) pr[t].d[i] = __ldg(D + (size_t)i * LN + jp);
       }
     }
   };
-  const uint32_t idesc = umma_idesc_s8u8(128, TC_COLS);
-  // one register buffer: the next chunk's digit reads are issued right after this chunk's key
-  // switching (their latency is covered by the other resident warps: 2 CTAs x 8 warps per SM)
-  load_chunk(0);
+  const uint32_t idesc = umma_idesc_s8u8(128, 8 * TC_COLS);  // one UMMA covers the 8 byte planes
+  // one register buffer (occupancy first: 2 CTAs x 12 warps per SM): the next chunk's digit
+  // reads are issued right after this chunk's key switching
+  Term* cur = pre;
+  load_chunk(0, pre);
+#pragma unroll 1
   for (int ch = 0; ch < nchunks; ch++) {
     const int s = ch % KT_STAGES;
-    const bool has_ks = 2 * ch + ks < nk32;
+    const bool has_ks = KT_KS * ch + ks < nk32;
     // weights: K step ws = tid >> 7 of this chunk, 2 x 16 B per thread
     const int ws = tid >> 7;
-    const bool has_w = 2 * ch + ws < nk32;
+    const bool has_w = KT_KS * ch + ws < nk32;
     uint4 wv = make_uint4(0, 0, 0, 0), wv2 = make_uint4(0, 0, 0, 0);
     if (has_w) {
-      const uint4* wp = reinterpret_cast<const uint4*>(wsrc + (size_t)(2 * ch + ws) * 4096) + (tid & 127);
+      const uint4* wp = reinterpret_cast<const uint4*>(wsrc + (size_t)(KT_KS * ch + ws) * 4096) + (tid & 127);
       wv = __ldg(wp);
       wv2 = __ldg(wp + 128);
     }
@@ -1260,29 +1277,18 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
     uint32_t lo0[4], hi0[4], lo1[4], hi1[4];
 #pragma unroll
     for (int t = 0; t < 4; t++) {
-      const int tap = pre[t].tap;
+      const int tap = cur[t].tap;
       u64 r0 = 0, r1 = 0;
       if (tap >= 0) {
-        const u64* key = s_key[tap];
-        if (key == nullptr) {
-          r0 = pre[t].c0;
-          r1 = pre[t].d[0];
+        r0 = cur[t].c0;
+        if (!s_haskey[tap]) {
+          r1 = cur[t].d[0];
         } else {
-          if (tap != ktap) {
-            const u64* kb = key + (size_t)l * N + j;
-            const size_t kblk = 2 * LT * LN;
-#pragma unroll
-            for (int x = 0; x < 2 * LT; x++) {
-              kv[x] = __ldg(kb + x * LN);
-              ksh[x] = __ldg(kb + x * LN + kblk);
-            }
-            ktap = tap;
-          }
-          r0 = pre[t].c0;
+          const u64* kp = skey + (size_t)tap * 4 * LT * TC_POS + pos;
 #pragma unroll
           for (int i = 0; i < LT; i++) {
-            r0 += shoup_mul(pre[t].d[i], kv[2 * i], ksh[2 * i], q);
-            r1 += shoup_mul(pre[t].d[i], kv[2 * i + 1], ksh[2 * i + 1], q);
+            r0 += shoup_mul(cur[t].d[i], kp[(4 * i) * TC_POS], kp[(4 * i + 1) * TC_POS], q);
+            r1 += shoup_mul(cur[t].d[i], kp[(4 * i + 2) * TC_POS], kp[(4 * i + 3) * TC_POS], q);
           }
         }
       }
@@ -1291,7 +1297,7 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
       lo1[t] = (uint32_t)r1;
       hi1[t] = (uint32_t)(r1 >> 32);
     }
-    if (ch + 1 < nchunks) load_chunk(ch + 1);
+    if (ch + 1 < nchunks) load_chunk(ch + 1, pre);
     uint32_t p0[8], p1[8];
     byte_tr4(lo0, p0);
     byte_tr4(hi0, p0 + 4);
@@ -1317,16 +1323,13 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
       if (prev % KT_WARPS == KT_WARPS - 1) {       // 8u .. 8u + 7; the last warp issues the UMMAs
         __threadfence_block();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        for (int k2 = 0; k2 < 2 && 2 * ch + k2 < nk32; k2++) {
+        for (int k2 = 0; k2 < KT_KS && KT_KS * ch + k2 < nk32; k2++) {
           const uint64_t da = umma_desc_kmajor(smem_u32(sA(s, k2)));
-#pragma unroll
-          for (int b = 0; b < 8; b++) {
-            const uint64_t db = umma_desc_kmajor(smem_u32(sB(s, k2, b)));
-            asm volatile(
-                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (uint32_t)(b * TC_COLS)),
-                "l"(da), "l"(db), "r"(idesc));
-          }
+          const uint64_t db = umma_desc_kmajor(smem_u32(sB(s, k2, 0)));  // all 8 planes: N = 256
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, 1, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem), "l"(da), "l"(db),
+              "r"(idesc));
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                          smem_u32(&empty_bar[s]))
@@ -1342,23 +1345,22 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   for (int ch = nchunks > KT_STAGES ? nchunks - KT_STAGES : 0; ch < nchunks; ch++)
     mbar_wait(&empty_bar[ch % KT_STAGES], (ch / KT_STAGES) & 1);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  {
+  if (warp < 8) {
     const int comp = chalf;
     const int row = mt * 128 + quad * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
-    for (int c0 = comp * 16; c0 < comp * 16 + 16; c0 += 8) {
-      uint32_t v[8][8];  // [plane][column]
+    for (int c0 = comp * 16; c0 < comp * 16 + 16; c0 += 4) {
+      uint32_t v[8][4];  // [plane][column]
 #pragma unroll
       for (int b = 0; b < 8; b++) {
-        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                     : "=r"(v[b][0]), "=r"(v[b][1]), "=r"(v[b][2]), "=r"(v[b][3]), "=r"(v[b][4]), "=r"(v[b][5]),
-                       "=r"(v[b][6]), "=r"(v[b][7])
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[b][0]), "=r"(v[b][1]), "=r"(v[b][2]), "=r"(v[b][3])
                      : "r"(lane_base + (uint32_t)(b * TC_COLS + c0)));
       }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int cc = 0; cc < 8; cc++) {
+      for (int cc = 0; cc < 4; cc++) {
         long long lo = 0, hi = 0;
 #pragma unroll
         for (int b = 0; b < 4; b++) lo += (long long)(int32_t)v[b][cc] << (8 * b);
@@ -1379,11 +1381,12 @@ hy_status launch_ksmac_tc(const KsMacArgs& a, const int8_t* w8, int units, cudaS
   const int N = 1 << a.logN;
   static bool attr_done = false;
   if (!attr_done) {
-    HY_CUDA_TRY(cudaFuncSetAttribute(ksmac_tc_kernel<LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)KT_SMEM));
+    HY_CUDA_TRY(cudaFuncSetAttribute(ksmac_tc_kernel<LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kt_smem(HY_MAX_TAPS, LT)));
     attr_done = true;
   }
   dim3 grid((unsigned)(a.L * (N / TC_POS)), (unsigned)((a.Mpad + 127) / 128), (unsigned)units);
-  ksmac_tc_kernel<LT><<<grid, KT_THREADS, KT_SMEM, s>>>(a, w8);
+  ksmac_tc_kernel<LT><<<grid, KT_THREADS, kt_smem(a.T, LT), s>>>(a, w8);
   HY_LAUNCH_CHECK();
   return HY_OK;
 }

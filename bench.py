@@ -272,7 +272,8 @@ MAC_KERNEL = {"thin": "ksmac_thin_kernel (fused S2+S3, FP64 MAC)",
               "tc_fused": "ksmac_tc_kernel (fused S2+S3: key switching + tcgen05 int8 MAC)",
               "tc_split": "mac_tc_kernel (S3 tcgen05 int8 MAC over stored R)",
               "fp64_fused": "ksmac_gemm_kernel (fused S2+S3, FP64 MAC)",
-              "fp64_split": "mac_gemm_kernel (S3 FP64 MAC over stored R)"}
+              "fp64_split": "mac_gemm_kernel (S3 FP64 MAC over stored R)",
+              "tc_coef": "mac_tc_kernel (1x1 c_n = 1: tcgen05 int8 MAC on the coefficient-form inputs, no NTT)"}
 
 
 def roofline(cfg, res, peaks, steps):
@@ -295,13 +296,17 @@ def roofline(cfg, res, peaks, steps):
     dom = max(st, key=st.get)
     kernels = {}
     for stage in ("S1_permdecomp", "S4S5_align_intt"):
+        if path == "tc_coef":       # 1x1 coefficient-domain MAC: no NTT stages at all
+            kernels[stage] = {"bound": "none", "achieved": 0.0, "peak": int_peak, "unit": "Gmodmul/s", "frac": 0.0,
+                              "ms": st[stage], "note": "empty stage (no NTT in the 1x1 c_n = 1 path)"}
+            continue
         a = w["modmul"][stage] / (st[stage] * 1e-3) / 1e9 if st[stage] > 0 else 0.0
         kernels[stage] = {"bound": "alu", "achieved": a, "peak": int_peak, "unit": "Gmodmul/s",
                           "frac": a / int_peak, "ms": st[stage]}
     if path in ("tc_fused", "thin"):
         a = w["modmul"]["S2S3_ksmac_wht"] / (mac_ms * 1e-3) / 1e9
         mac = {"bound": "alu", "achieved": a, "peak": int_peak, "unit": "Gmodmul/s", "frac": a / int_peak}
-    elif path == "tc_split":
+    elif path in ("tc_split", "tc_coef"):
         hbm = peaks.get("hbm_gbs", 6546.6)
         a = (w["r_bytes"] + w["out_bytes"] * (2 if lay.cn == 2 and not cfg.depthwise else 1)) / (mac_ms * 1e-3) / 1e9
         mac = {"bound": "hbm", "achieved": a, "peak": hbm, "unit": "GB/s", "frac": a / hbm}

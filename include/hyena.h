@@ -161,11 +161,13 @@ hy_status hy_weights_mac_time(const hy_weights* w, float* total_ms, uint32_t* la
 
 /* Kernel choice for S2 + S3, fixed by hy_encode_weights from the layout:
  *   0 HY_MAC_THIN        depthwise: key switching fused into a thin FP64 MAC;
- *   1 HY_MAC_TC_FUSED    dense, M <= 128 MAC rows, L in {2,3,5}: key switching in the producer
+ *   1 HY_MAC_TC_FUSED    dense, 32 < M <= 128 MAC rows, L in {2,3,5}: key switching in the producer
  *                        warps of the tcgen05 int8 MAC (rotated inputs never stored);
  *   2 HY_MAC_TC_SPLIT    dense: PermAuto materialises the rotated inputs, tcgen05 MAC reads them;
- *   3 HY_MAC_FP64_FUSED  dense, M <= 32: key switching + FP64 DFMA MAC (30-bit halves);
- *   4 HY_MAC_FP64_SPLIT  dense, M > 32: PermAuto + FP64 DFMA MAC.
+ *   3 HY_MAC_FP64_FUSED  dense, M <= 32 (default there): key switching + FP64 DFMA MAC (30-bit halves);
+ *   4 HY_MAC_FP64_SPLIT  dense, M > 32: PermAuto + FP64 DFMA MAC;
+ *   5 HY_MAC_TC_COEF     1x1 kernel, pad 0, c_n = 1: tcgen05 MAC directly on the coefficient-form
+ *                        inputs (identity tap, linear MAC), no NTT / INTT at all.
  * Every path computes the same bits (the MAC is exact integer arithmetic).  set_mac_path selects
  * another valid path for A/B measurement and parity tests (allocates the rotated-input workspace
  * of the split paths).  Errors: HY_EINVAL (path not valid for this layout), HY_ENOMEM. */

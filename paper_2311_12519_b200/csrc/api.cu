@@ -408,6 +408,11 @@ extern "C" hy_status hy_keys_upload(hy_params* p, uint32_t n, const uint32_t* el
 // ============================================================================================
 // weights
 // ============================================================================================
+// 1x1 kernel, no padding, c_n = 1, dense: the coefficient-domain MAC applies (HY_MAC_TC_COEF)
+static bool coef_ok(const hy_weights* w, const hy_layout& lay) {
+  return !w->shape.depthwise && lay.n_taps == 1 && lay.tap_step[0] == 0 && lay.cn == 1;
+}
+
 extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, const int8_t* Wt, hy_weights** out) {
   HY_CHECK(p && sh && Wt && out, HY_EINVAL, "null argument");
   hy_layout lay;
@@ -431,7 +436,7 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
     w->wblocks = 1;
   }
   w->Mpad = hy_mac_mpad(w->M);
-  w->mac_path = hy_mac_path(w->M, (int)p->L, dw);
+  w->mac_path = hy_mac_path(w->M, (int)p->L, dw, coef_ok(w, lay));
   w->Kpad = (w->K + 31) / 32 * 32;  // multiple of the MAC K chunks (16 FP64 GEMM, 32 tcgen05)
   // weight table (S0), [block][kk][row] as exact doubles; row semantics documented in DESIGN.md §4
   std::vector<double> wt((size_t)w->wblocks * w->Kpad * w->Mpad, 0.0);
@@ -588,6 +593,7 @@ extern "C" hy_status hy_weights_set_mac_path(hy_weights* w, int32_t path) {
     case HY_MAC_TC_SPLIT: ok = !dw; break;
     case HY_MAC_FP64_SPLIT: ok = !dw && w->M > 32; break;  // 64-row FP64 tiles (hy_mac_mpad)
     case HY_MAC_FP64_FUSED: ok = !dw && w->M <= 32; break;
+    case HY_MAC_TC_COEF: ok = coef_ok(w, w->lay); break;
   }
   HY_CHECK(ok, HY_EINVAL, "MAC path %d is not valid for this layout (M = %d, L = %d, depthwise = %d)", path, w->M, L,
            (int)dw);
@@ -659,6 +665,10 @@ static hy_status bind_keys(hy_weights* w) {
     HY_CHECK(it != p->keys.end(), HY_ENOKEY, "no Galois key for the row swap (element %u)", 2 * p->N - 1);
     w->d_swap_key = it->second.ntt;
   }
+  for (uint32_t tau = 0; tau < lay.n_taps; tau++) {
+    w->h_tap_keys[tau] = ptrs[tau];
+    w->h_tap_act[tau] = acts[tau];
+  }
   HY_CUDA_TRY(cudaMemcpy(w->d_tap_keys, ptrs.data(), ptrs.size() * sizeof(u64*), cudaMemcpyHostToDevice));
   HY_CUDA_TRY(cudaMemcpy(w->d_tap_act, acts.data(), acts.size() * sizeof(GaloisAct), cudaMemcpyHostToDevice));
   w->keys_version = p->keys_version;
@@ -685,6 +695,13 @@ extern "C" hy_status hy_conv_eval(hy_weights* w, const uint64_t* ct_in, size_t J
     return HY_OK;
   };
   HY_TRY(mark(0));
+  if (w->mac_path == HY_MAC_TC_COEF) {  // 1x1, c_n = 1: one MAC over the coefficient-form inputs
+    HY_TRY(mark(1));
+    HY_TRY(hyk::mac_coef(w, ct_in, nu, ct_out, s));
+    HY_TRY(mark(2));
+    HY_TRY(mark(3));
+    return HY_OK;
+  }
   HY_TRY(hyk::permdecomp(p, ct_in, J, w->d_D, w->d_C0, s));  // S1 PermDecomp
   HY_TRY(mark(1));
   HY_TRY(hyk::ksmac(w, nu, s));  // S2 PermAuto fused with S3 lazy MAC + WHT + reduce + sign PMult

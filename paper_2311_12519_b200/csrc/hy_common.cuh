@@ -126,8 +126,9 @@ enum HyMacPath {
   HY_MAC_TC_SPLIT = 2,    // dense, M > 128: PermAuto materialises R, tcgen05 MAC consumes it
   HY_MAC_FP64_FUSED = 3,  // A/B option HY_MAC_FP64 (M <= 32): key switching + FP64 DFMA MAC
   HY_MAC_FP64_SPLIT = 4,  // A/B option HY_MAC_FP64 (M > 32): PermAuto + FP64 DFMA MAC
+  HY_MAC_TC_COEF = 5,     // 1x1, c_n = 1: tcgen05 MAC straight on the coefficient-form inputs, no NTT
 };
-int hy_mac_path(int M, int L, bool depthwise);
+int hy_mac_path(int M, int L, bool depthwise, bool coef_ok);
 
 struct hy_weights {
   hy_params* p;
@@ -155,6 +156,8 @@ struct hy_weights {
   u64* d_in;        // staging for hy_conv_eval_host
   u64* d_out;
   u64** d_tap_keys;            // device array of key pointers per tap (nullptr = identity)
+  u64* h_tap_keys[HY_MAX_TAPS];       // the same tables on the host (passed by value to kernels)
+  GaloisAct h_tap_act[HY_MAX_TAPS];
   GaloisAct* d_tap_act;        // device array of slot-order automorphism actions per tap
   u64* d_swap_key;
   u64 keys_version;            // params->keys_version the tap table was built from
@@ -209,6 +212,7 @@ hy_status key_to_ntt(const hy_params* p, const u64* key_coeff, u64* key_ntt, cud
 hy_status permdecomp(const hy_params* p, const u64* ct, size_t nct, u64* D, u64* C0, cudaStream_t s);
 hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s);  // S2 + S3
 hy_status finish_outputs(const hy_weights* w, size_t nunits, u64* ct_out, cudaStream_t s);
+hy_status mac_coef(hy_weights* w, const u64* ct_in, size_t nunits, u64* ct_out, cudaStream_t s);
 hy_status rotate_ct(const hy_params* p, const u64* ct_in, GaloisAct act, const u64* key, u64* ct_out, size_t n,
                     u64* work, cudaStream_t s);
 hy_status decrypt_phase(const hy_params* p, const u64* s_ntt, const u64* s_ntt_sh, const u64* ct, size_t n,

@@ -382,6 +382,10 @@ struct KsMacArgs {
   u64* out;                    // [z][M'][2][L][N], M' = M (cn 1) or M/2 (cn 2)
   const u64* sign;             // [L][N] sign plaintext (NTT), then [L][N] Shoup companions
   const int32_t* kt;           // fused tensor-core MAC: K term -> (tap << 16) | ct (-1 = padding)
+  struct Taps {                // key pointers + automorphisms per tap, by value (no pointer chase)
+    const u64* key[HY_MAX_TAPS];
+    GaloisAct act[HY_MAX_TAPS];
+  } tt;
   int T, Jcb, K, Kpad, M, Mpad, wblocks, L, logN, kscale, cn;
   LimbConsts lcs;
 };
@@ -1174,14 +1178,14 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   for (int t = tid; t < a.T; t += KT_THREADS) {
-    s_haskey[t] = a.keys[t] != nullptr;
-    s_act[t] = a.act[t];
+    s_haskey[t] = a.tt.key[t] != nullptr;
+    s_act[t] = a.tt.act[t];
   }
   // stage the key words of this CTA (limb l, positions j0 .. j0 + 15) for every tap
   for (int e = tid; e < a.T * 4 * LT * TC_POS; e += KT_THREADS) {
     const int p = e % TC_POS, r = e / TC_POS;
     const int sh = r % 2, x = (r / 2) % (2 * LT), tap = r / (4 * LT);
-    const u64* key = a.keys[tap];
+    const u64* key = a.tt.key[tap];
     skey[e] = key ? __ldg(key + (size_t)sh * 2 * LT * LN + (size_t)x * LN + (size_t)l * N + j0 + p) : 0ull;
   }
   if (tid < KT_STAGES) s_ticket[tid] = 0;
@@ -1528,6 +1532,10 @@ hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
   a.C0 = w->d_C0;
   a.keys = w->d_tap_keys;
   a.act = w->d_tap_act;
+  for (uint32_t t = 0; t < lay.n_taps && t < HY_MAX_TAPS; t++) {
+    a.tt.key[t] = w->h_tap_keys[t];
+    a.tt.act[t] = w->h_tap_act[t];
+  }
   a.wt = w->d_wt;
   a.out = w->d_P;
   a.sign = w->d_sign;
@@ -1597,6 +1605,37 @@ hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
     if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[2 * w->mac_launches + 1], s));
     w->mac_launches++;
   }
+  return HY_OK;
+}
+
+// 1x1 convolution with c_n = 1 (SURVEY §8(a) special case): the only tap is
+// the identity, so the hoisted rotation is the input itself and the MAC is linear: computing
+// Out_o = sum_c W[o][c] ct_c on the coefficient-form inputs and reducing once gives the same
+// canonical residues as NTT -> MAC -> INTT, with no NTT at all.  The tensor-core MAC reads the
+// input ciphertexts [unit][c][2][L][N] as its R operand and writes ct_out [unit][o][2][L][N].
+hy_status mac_coef(hy_weights* w, const u64* ct_in, size_t nunits, u64* ct_out, cudaStream_t s) {
+  w->mac_launches = 0;
+  const hy_params* p = w->p;
+  KsMacArgs a;
+  a.out = ct_out;
+  a.sign = nullptr;
+  a.T = 1;
+  a.Jcb = (int)w->lay.Jc;
+  a.K = w->K;
+  a.Kpad = w->Kpad;
+  a.M = w->M;
+  a.Mpad = w->Mpad;
+  a.wblocks = w->wblocks;
+  a.L = (int)p->L;
+  a.logN = (int)p->logN;
+  a.kscale = 1;
+  a.cn = 1;
+  a.lcs = limb_consts(p);
+  HY_TRY(mac_mark(w, s));
+  if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[0], s));
+  HY_TRY(launch_mac_tc(a, ct_in, w->d_w8, (int)nunits, s));
+  if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[1], s));
+  w->mac_launches = 1;
   return HY_OK;
 }
 
@@ -1678,11 +1717,15 @@ hy_status decrypt_phase(const hy_params* p, const u64* s_ntt, const u64* s_ntt_s
 
 }  // namespace hyk
 
-int hy_mac_path(int M, int L, bool depthwise) {
+int hy_mac_path(int M, int L, bool depthwise, bool coef_ok) {
   if (depthwise) return HY_MAC_THIN;
   static const bool fp64 = getenv("HY_MAC_FP64") != nullptr;    // A/B switches
   static const bool split = getenv("HY_SPLIT_TC") != nullptr;
+  if (coef_ok && !fp64 && !split) return HY_MAC_TC_COEF;
   if (fp64) return M <= 32 ? HY_MAC_FP64_FUSED : HY_MAC_FP64_SPLIT;
+  // M <= 32 (latency-bound small layers, e.g. C1/C2): the FP64 fused kernel is faster (measured,
+  // DESIGN.md §4); 32 < M <= 128: key switching fused into the tcgen05 MAC
+  if (!split && M <= 32) return HY_MAC_FP64_FUSED;
   if (!split && M <= 128 && (L == 2 || L == 3 || L == 5)) return HY_MAC_TC_FUSED;
   return HY_MAC_TC_SPLIT;
 }

@@ -30,7 +30,7 @@ EXPORTED = ["hy_last_error", "hy_plan_layout", "hy_params_create", "hy_params_de
             "hy_weights_set_stage_events", "hy_weights_mac_time", "hy_weights_mac_path", "hy_weights_set_mac_path"]
 
 # S2 + S3 kernel choices (include/hyena.h hy_weights_mac_path)
-MAC_PATHS = {"thin": 0, "tc_fused": 1, "tc_split": 2, "fp64_fused": 3, "fp64_split": 4}
+MAC_PATHS = {"thin": 0, "tc_fused": 1, "tc_split": 2, "fp64_fused": 3, "fp64_split": 4, "tc_coef": 5}
 
 
 class HyenaError(RuntimeError):

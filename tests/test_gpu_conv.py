@@ -101,7 +101,7 @@ CASES = {
 }
 
 
-PATHS = ["default", "tc_fused", "tc_split", "fp64_fused", "fp64_split", "thin"]
+PATHS = ["default", "tc_fused", "tc_split", "fp64_fused", "fp64_split", "thin", "tc_coef"]
 
 
 @pytest.mark.parametrize("path", PATHS)

@@ -567,29 +567,113 @@ template <int WM, int LT>
 __global__ void __launch_bounds__(256, 2) ksmac_gemm_kernel(KsMacArgs a) {
   constexpr int BM = 8 * WM, PG = 8 / WM, BNP = 32 * PG, KC = 2 * WM;
   static_assert(KC * BNP == 512, "two R items per thread per chunk");
+  constexpr int NL = LT > 0 ? LT : 1;
   extern __shared__ __align__(16) unsigned char smraw[];
   auto Rs = reinterpret_cast<double2(*)[KC][2][BNP]>(smraw);                                // [2][KC][2][BNP]
   auto Ws = reinterpret_cast<double(*)[KC][BM]>(smraw + sizeof(double2) * 2 * KC * 2 * BNP);  // [2][KC][BM]
+  // LT > 0: key words of this CTA (limb l, BNP positions) for every tap, staged once:
+  // [tap][x = 2 digit + comp][2: value, Shoup][BNP]
+  u64* skey = reinterpret_cast<u64*>(smraw + sizeof(double2) * 2 * KC * 2 * BNP + sizeof(double) * 2 * KC * BM);
   __shared__ const u64* s_key[HY_MAX_TAPS];
   __shared__ GaloisAct s_act[HY_MAX_TAPS];
 
   const int N = 1 << a.logN;
+  const size_t LNs = (size_t)(LT > 0 ? LT : a.L) * N;
   const int tiles = N / BNP;
   const int l = blockIdx.x / tiles, j0 = (blockIdx.x % tiles) * BNP;
   const int row0 = blockIdx.y * BM, z = blockIdx.z;
   const double* __restrict__ wt = a.wt + (size_t)(z % a.wblocks) * a.Kpad * a.Mpad;
   const LimbConst cst = a.lcs.lc[l];
   for (int t = threadIdx.x; t < a.T; t += 256) {
-    s_key[t] = a.keys[t];
-    s_act[t] = a.act[t];
+    s_key[t] = a.tt.key[t];
+    s_act[t] = a.tt.act[t];
+  }
+  if constexpr (LT > 0) {
+    for (int e = threadIdx.x; e < a.T * 4 * LT * BNP; e += 256) {
+      const int pp = e % BNP, r = e / BNP;
+      const int sh = r % 2, x = (r / 2) % (2 * LT), tap = r / (4 * LT);
+      const u64* key = a.tt.key[tap];
+      skey[e] = key ? __ldg(key + (size_t)sh * 2 * LT * LNs + (size_t)x * LNs + (size_t)l * N + j0 + pp) : 0ull;
+    }
   }
   __syncthreads();
 
   // Every thread produces the items (kkl, p) = (tid / BNP + 256 h / BNP, tid % BNP), h = 0, 1:
-  // always the same position p, so the tap keys stay in registers across items and chunks.
+  // always the same position p.  LT > 0: the digit reads of chunk ch + 1 are issued before the
+  // DFMAs of chunk ch (register prefetch) and switched after them, keys come from shared memory.
   constexpr int WPT = (KC * BM + 255) / 256;  // weights staged per thread per chunk
   KeyRegs<LT> kr;
-  auto produce = [&](int chunk, int buf) {
+  const int p_own = threadIdx.x % BNP;
+  const int jp_own = j0 + p_own;
+  const float inv_jc = 1.0f / (float)a.Jcb;
+  struct Pre {
+    u64 c0, d[NL];
+    int tap;
+  } pre[2];
+  double wpre[WPT];
+  auto issue = [&](int chunk) {  // LT > 0: loads of chunk `chunk` into registers
+#pragma unroll
+    for (int u = 0; u < WPT; u++) {
+      const int it = threadIdx.x + 256 * u;
+      if (it < KC * BM) wpre[u] = __ldg(wt + (size_t)(chunk * KC + it / BM) * a.Mpad + row0 + it % BM);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int it = threadIdx.x + 256 * h;
+      const int kk = chunk * KC + it / BNP;
+      pre[h].tap = -1;
+      if (kk >= a.K) continue;
+      int tap = (int)((float)kk * inv_jc);  // kk / Jcb (kk < 2^16: off by at most one)
+      if (tap * a.Jcb > kk) tap--;
+      if ((tap + 1) * a.Jcb <= kk) tap++;
+      const int c = kk - tap * a.Jcb;
+      pre[h].tap = tap;
+      const size_t ct = (size_t)z * a.Jcb + c;
+      const u64* C0 = a.C0 + ct * LNs + (size_t)l * N;
+      const u64* D = a.D + ct * NL * LNs + (size_t)l * N;
+      if (s_key[tap] == nullptr) {
+        pre[h].c0 = __ldg(C0 + jp_own);
+        pre[h].d[0] = __ldg(D + (size_t)l * LNs + jp_own);
+      } else {
+        const int jp = galois_perm(jp_own, s_act[tap], N >> 1);
+        pre[h].c0 = __ldg(C0 + jp);
+#pragma unroll
+        for (int i = 0; i < NL; i++) pre[h].d[i] = __ldg(D + (size_t)i * LNs + jp);
+      }
+    }
+  };
+  auto finish = [&](int buf) {  // LT > 0: key-switch the prefetched items into Rs[buf], Ws[buf]
+    const u64 q = cst.q, q2 = cst.two_q;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      const int kkl = (threadIdx.x + 256 * h) / BNP;
+      u64 r0 = 0, r1 = 0;
+      const int tap = pre[h].tap;
+      if (tap >= 0) {
+        r0 = pre[h].c0;
+        if (s_key[tap] == nullptr) {
+          r1 = pre[h].d[0];
+        } else {
+          const u64* kp = skey + (size_t)tap * 4 * NL * BNP + p_own;
+#pragma unroll
+          for (int i = 0; i < NL; i++) {
+            r0 = csub(r0 + shoup_mul(pre[h].d[i], kp[(4 * i) * BNP], kp[(4 * i + 1) * BNP], q), q2);
+            r1 = csub(r1 + shoup_mul(pre[h].d[i], kp[(4 * i + 2) * BNP], kp[(4 * i + 3) * BNP], q), q2);
+          }
+          r0 = csub(r0, q);  // canonical: the 30-bit split needs R < 2^60
+          r1 = csub(r1, q);
+        }
+      }
+      Rs[buf][kkl][0][p_own] = make_double2((double)(uint32_t)(r0 >> 30), (double)(uint32_t)(r0 & M30));
+      Rs[buf][kkl][1][p_own] = make_double2((double)(uint32_t)(r1 >> 30), (double)(uint32_t)(r1 & M30));
+    }
+#pragma unroll
+    for (int u = 0; u < WPT; u++) {
+      const int it = threadIdx.x + 256 * u;
+      if (it < KC * BM) Ws[buf][it / BM][it % BM] = wpre[u];
+    }
+  };
+  auto produce = [&](int chunk, int buf) {  // LT == 0: generic L, loads + switching in one go
     double wv[WPT];
 #pragma unroll
     for (int u = 0; u < WPT; u++) {
@@ -622,11 +706,19 @@ __global__ void __launch_bounds__(256, 2) ksmac_gemm_kernel(KsMacArgs a) {
     for (int n = 0; n < 2; n++) acc_h[r][n] = acc_l[r][n] = 0.0;
 
   const int nchunks = a.Kpad / KC;
-  produce(0, 0);
+  if constexpr (LT > 0) {
+    issue(0);
+    finish(0);
+    if (nchunks > 1) issue(1);
+  } else {
+    produce(0, 0);
+  }
   __syncthreads();
   for (int ch = 0; ch < nchunks; ch++) {
     const int buf = ch & 1;
-    if (ch + 1 < nchunks) produce(ch + 1, buf ^ 1);
+    if constexpr (LT == 0) {
+      if (ch + 1 < nchunks) produce(ch + 1, buf ^ 1);
+    }
 #pragma unroll
     for (int kkl = 0; kkl < KC; kkl++) {
       const double2* wp = reinterpret_cast<const double2*>(&Ws[buf][kkl][rg * 8]);
@@ -644,6 +736,12 @@ __global__ void __launch_bounds__(256, 2) ksmac_gemm_kernel(KsMacArgs a) {
         acc_l[r][0] = fma(w[r], x0.y, acc_l[r][0]);
         acc_h[r][1] = fma(w[r], x1.x, acc_h[r][1]);
         acc_l[r][1] = fma(w[r], x1.y, acc_l[r][1]);
+      }
+    }
+    if constexpr (LT > 0) {
+      if (ch + 1 < nchunks) {
+        finish(buf ^ 1);                     // chunk ch + 1 (its reads were in flight)
+        if (ch + 2 < nchunks) issue(ch + 2);
       }
     }
     __syncthreads();
@@ -1428,18 +1526,28 @@ hy_status launch_permauto(const KsMacArgs& a, u64* R, int units, cudaStream_t s)
 }
 
 template <int WM, int LT>
-hy_status launch_ksmac_gemm(const KsMacArgs& a, int units, cudaStream_t s) {
+hy_status launch_ksmac_gemm_t(const KsMacArgs& a, int units, cudaStream_t s) {
   const int N = 1 << a.logN, BNP = 256 / WM, KC = 2 * WM;
-  const size_t sm = sizeof(double2) * 2 * KC * 2 * BNP + sizeof(double) * 2 * KC * 8 * WM;
-  static bool attr_done = false;
-  if (!attr_done) {
+  const size_t sm0 = sizeof(double2) * 2 * KC * 2 * BNP + sizeof(double) * 2 * KC * 8 * WM;
+  const size_t sm = sm0 + (LT > 0 ? (size_t)a.T * 4 * LT * BNP * sizeof(u64) : 0);
+  static size_t attr = 0;
+  if (sm > attr) {
     HY_CUDA_TRY(cudaFuncSetAttribute(ksmac_gemm_kernel<WM, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr_done = true;
+    attr = sm;
   }
   dim3 grid((unsigned)(a.L * (N / BNP)), (unsigned)(a.Mpad / (8 * WM)), (unsigned)units);
   ksmac_gemm_kernel<WM, LT><<<grid, 256, sm, s>>>(a);
   HY_LAUNCH_CHECK();
   return HY_OK;
+}
+
+// the key-staging variant (LT > 0) while its shared memory stays <= 100 KB (2 CTAs per SM), else
+// the generic one (keys through L1)
+template <int WM, int LT>
+hy_status launch_ksmac_gemm(const KsMacArgs& a, int units, cudaStream_t s) {
+  const size_t keys = (size_t)a.T * 4 * (LT > 0 ? LT : 1) * (256 / WM) * sizeof(u64);
+  if (LT > 0 && keys <= 64 * 1024) return launch_ksmac_gemm_t<WM, LT>(a, units, s);
+  return launch_ksmac_gemm_t<WM, 0>(a, units, s);
 }
 
 template <int MR, int LT>

@@ -24,16 +24,17 @@ for f in sorted(glob.glob("gpurun_out/bench_*.log")):
             name = os.path.basename(f)[6:-4]
             bench[name] = d
 json.dump(bench, open(f"profiles/{tag}_bench.json", "w"), indent=1)
-out_md.append("## bench.py lines\n\n| run | value | ms/step | S1 | S2+S3 (ksmac) | S4+S5 | ksmac frac of FP64 peak | e2e | clocks |\n|---|---|---|---|---|---|---|---|---|")
+out_md.append("## bench.py lines\n\n| run | value | ms/step | MAC path | S1 ms | S2+S3 ms | S4+S5 ms | dominant stage: kernel, achieved / peak (frac) | e2e | clocks |\n|---|---|---|---|---|---|---|---|---|---|")
 for n, d in bench.items():
     if "roofline" not in d:
-        out_md.append(f"| {n} (reference arm) | {d['value']:.4g} {d['unit']} | {d['ms_per_step']:.1f} | | | | | | |")
+        out_md.append(f"| {n} (reference arm) | {d['value']:.4g} {d['unit']} | {d['ms_per_step']:.1f} | | | | | | | |")
         continue
     st = d["stages_ms"]
     r = d["roofline"] or {}
-    out_md.append(f"| {n} | {d['value']:.1f} {d['unit']} | {d['ms_per_step']:.3f} | {st['S1_permdecomp']:.3f} | "
-                  f"{st['S2S3_ksmac_wht']:.3f} | {st['S4S5_align_intt']:.3f} | {r.get('frac', 0):.3f} | "
-                  f"{d['e2e']['value']:.1f} | {d['clocks']['sm_mhz']} MHz {d['clocks']['reasons']} |")
+    out_md.append(f"| {n} | {d['value']:.1f} {d['unit']} | {d['ms_per_step']:.3f} | {d.get('mac_path')} | "
+                  f"{st['S1_permdecomp']:.3f} | {st['S2S3_ksmac_wht']:.3f} | {st['S4S5_align_intt']:.3f} | "
+                  f"{r.get('dominant_stage')}: {r.get('kernel', '')[:40]}, {r.get('achieved', 0):.1f} / {r.get('peak', 0):.1f} "
+                  f"{r.get('unit', '')} ({r.get('frac', 0):.3f}) | {d['e2e']['value']:.1f} | {d['clocks']['sm_mhz']} MHz {d['clocks']['reasons']} |")
 
 # launch lists
 for f in sorted(glob.glob("gpurun_out/launches_*.csv")):
@@ -75,15 +76,17 @@ for f in sorted(glob.glob("gpurun_out/prof_*_full.ncu-rep")):
             i = hdr.index(c)
             vals.append(f"{r[i]} {units[i]}".strip())
         out_md.append(f"| `{name[:60]}` | " + " | ".join(vals) + " |")
-        if "mac" in name:
+        stage = ("S2S3_ksmac_wht" if "mac" in name else "S1_permdecomp" if "PermDecomp" in name else
+                 "S4S5_align_intt" if any(k in name for k in ("OutInv", "StridedInv", "DigitLift", "ks_apply")) else None)
+        if stage:   # dram bytes per launch, summed over the stage's kernels (one launch of each captured)
             i_r, i_w = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             b = float(r[i_r].replace(",", "")) * scale.get(units[i_r], 1) + \
                 float(r[i_w].replace(",", "")) * scale.get(units[i_w], 1)
-            traffic.setdefault(cfg, {}).setdefault("mac", 0.0)
-            traffic[cfg]["mac"] = max(traffic[cfg]["mac"], b)
+            traffic.setdefault(cfg, {}).setdefault(stage, {})[name.split("::")[-1][:40]] = b
     os.system(f"cp {f} profiles/{tag}_{os.path.basename(f)[5:]}")
 if traffic:
+    traffic = {c: {st: sum(v.values()) for st, v in d.items()} for c, d in traffic.items()}
     json.dump(traffic, open("profiles/traffic.json", "w"), indent=1)
 open(f"profiles/{tag}_summary.md", "w").write("\n".join(out_md) + "\n")
 print("\n".join(out_md))

@@ -1052,11 +1052,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   }
 }
 
+template <int LT = 0, int LOGN = 0>
 __device__ __forceinline__ void tc_store(const KsMacArgs& a, int z, int row, int comp, int l, int j, long long H,
                                          long long Lo) {
   // this lane holds B = H 2^32 + Lo for MAC row `row` (|H|, |Lo| < 2^56); lanes row^1 pair up
-  const int N = 1 << a.logN;
-  const size_t LN = (size_t)a.L * N;
+  const int N = LOGN > 0 ? (1 << LOGN) : (1 << a.logN);
+  const size_t LN = (size_t)(LT > 0 ? LT : a.L) * N;
   const LimbConst& c = a.lcs.lc[l];
   auto red = [&](long long h, long long lo) -> u64 {  // |h|, |lo| < 2^62
     const u64 hu = (u64)(h + (long long)c.off62), lu = (u64)(lo + (long long)c.off62);
@@ -1249,7 +1250,7 @@ constexpr int KT_STAGE_A = KT_KS * 4096, KT_STAGE_B = KT_KS * 8 * 1024;
 constexpr size_t KT_SMEM_MMA = (size_t)KT_STAGES * (KT_STAGE_A + KT_STAGE_B) + 1024;
 inline size_t kt_smem(int T, int L) { return KT_SMEM_MMA + (size_t)T * 4 * L * TC_POS * sizeof(u64); }
 
-template <int LT>
+template <int LT, int LOGN>  // LOGN > 0: compile-time ring degree (address math folds into immediates)
 __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, const int8_t* __restrict__ w8) {
   extern __shared__ uint8_t kt_dyn[];
   uint8_t* smb = reinterpret_cast<uint8_t*>(((uintptr_t)kt_dyn + 1023) & ~(uintptr_t)1023);
@@ -1265,8 +1266,9 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   __shared__ int s_haskey[HY_MAX_TAPS];
   __shared__ GaloisAct s_act[HY_MAX_TAPS];
 
-  const int N = 1 << a.logN;
-  const size_t LN = (size_t)LT * N;
+  constexpr bool CN = LOGN > 0;
+  const int N = CN ? (1 << LOGN) : (1 << a.logN);
+  const int LN = LT * N;  // < 2^31
   const int tiles = N / TC_POS;
   const int l = blockIdx.x / tiles, j0 = (blockIdx.x % tiles) * TC_POS;
   const int mt = blockIdx.y, z = blockIdx.z;
@@ -1274,6 +1276,61 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   const int nk32 = a.Kpad / 32;
   const int nchunks = (nk32 + KT_KS - 1) / KT_KS;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  // ---------------- producers (all warps) ----------------
+  const int pos = tid & 15, tg = tid >> 4;  // position; terms 4 tg .. 4 tg + 3 of each chunk
+  const int ks = tg >> 3, kg = tg & 7;
+  const int j = j0 + pos;
+  const u64 q = a.lcs.lc[l].q;
+  const int8_t* wsrc = w8 + ((size_t)(z % a.wblocks) * nmt + mt) * nk32 * 4096;
+  const u64* C0u = a.C0 + (size_t)z * a.Jcb * LN + (size_t)l * N;
+  const u64* Du = a.D + (size_t)z * a.Jcb * LT * LN + (size_t)l * N;
+  // K-major canonical plane offsets of column pos (c0) and 16 + pos (c1), terms 4kg .. 4kg + 3
+  const int off0 = (pos >> 3) * 256 + (kg >> 2) * 128 + (pos & 7) * 16 + (kg & 3) * 4;
+  const int off1 = off0 + 2 * 256;
+  // (tap, c) of this thread's first term of the current chunk, advanced incrementally (no division)
+  int tap0 = 0, c0t = tg * 4;
+  while (c0t >= a.Jcb) {
+    c0t -= a.Jcb;
+    tap0++;
+  }
+  struct Term {
+    u64 c0, d[LT];
+    int tap;  // -1 = padding term (R = 0); identity tap: d[0] = D_{c,l}
+  };
+  Term pre[4];
+  auto load_chunk = [&](int ch, Term* pr) {
+    int tap = tap0, c = c0t;
+#pragma unroll
+    for (int t = 0; t < 4; t++) {
+      if (t > 0 && ++c >= a.Jcb) {
+        c = 0;
+        tap++;
+      }
+      const int kk = ch * KT_CHUNK + tg * 4 + t;
+      pr[t].tap = -1;
+      if (kk >= a.K) continue;
+      pr[t].tap = tap;
+      const u64* C0 = C0u + (size_t)c * LN;
+      const u64* D = Du + (size_t)c * (LT * LN);
+      if (a.tt.key[tap] == nullptr) {  // identity tap: R = (C0_c, D_{c,l}) in limb l
+        pr[t].c0 = __ldg(C0 + j);
+        pr[t].d[0] = __ldg(D + l * LN + j);
+      } else {
+        const u64* Dp = D + galois_perm(j, a.tt.act[tap], N >> 1);
+        pr[t].c0 = __ldg(C0 + (Dp - D));
+#pragma unroll
+        for (int i = 0; i < LT; i++) pr[t].d[i] = __ldg(Dp + i * LN);
+      }
+    }
+    c0t += KT_CHUNK;  // advance to the next chunk's first term
+    while (c0t >= a.Jcb) {
+      c0t -= a.Jcb;
+      tap0++;
+    }
+  };
+  // the first chunk's digit reads are in flight while the keys are staged and TMEM is set up
+  load_chunk(0, pre);
 
   for (int t = tid; t < a.T; t += KT_THREADS) {
     s_haskey[t] = a.tt.key[t] != nullptr;
@@ -1301,7 +1358,8 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
   const int quad = warp & 3, chalf = warp >> 2;  // TMEM lanes 32 quad .. and columns half chalf
-  if (warp < 8) {
+  const bool rows_live = mt * 128 + quad * 32 < a.M;  // rows >= M are padding: never read back
+  if (warp < 8 && rows_live) {
     const uint32_t zb = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(chalf * TC_TMEM_COLS / 2);
     const uint32_t z0 = 0;
 #pragma unroll 1
@@ -1313,52 +1371,10 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
 
-  // ---------------- producers (all warps) ----------------
-  const int pos = tid & 15, tg = tid >> 4;  // position; terms 4 tg .. 4 tg + 3 of each chunk
-  const int ks = tg >> 3, kg = tg & 7;
-  const int j = j0 + pos;
-  const u64 q = a.lcs.lc[l].q;
-  const int8_t* wsrc = w8 + ((size_t)(z % a.wblocks) * nmt + mt) * nk32 * 4096;
-  const u64* C0u = a.C0 + (size_t)z * a.Jcb * LN + (size_t)l * N;
-  const u64* Du = a.D + (size_t)z * a.Jcb * LT * LN + (size_t)l * N;
-  // K-major canonical plane offsets of column pos (c0) and 16 + pos (c1), terms 4kg .. 4kg + 3
-  const int off0 = (pos >> 3) * 256 + (kg >> 2) * 128 + (pos & 7) * 16 + (kg & 3) * 4;
-  const int off1 = off0 + 2 * 256;
-  const float inv_jc = 1.0f / (float)a.Jcb;
-  struct Term {
-    u64 c0, d[LT];
-    int tap;  // -1 = padding term (R = 0); identity tap: d[0] = D_{c,l}
-  };
-  Term pre[4];
-  auto load_chunk = [&](int ch, Term* pr) {
-#pragma unroll
-    for (int t = 0; t < 4; t++) {
-      const int kk = ch * KT_CHUNK + tg * 4 + t;
-      pr[t].tap = -1;
-      if (kk >= a.K) continue;
-      int tap = (int)((float)kk * inv_jc);  // kk / Jcb (kk < 2^16: off by at most one)
-      if (tap * a.Jcb > kk) tap--;
-      if ((tap + 1) * a.Jcb <= kk) tap++;
-      const int c = kk - tap * a.Jcb;
-      pr[t].tap = tap;
-      const u64* C0 = C0u + (size_t)c * LN;
-      const u64* D = Du + (size_t)c * LT * LN;
-      if (!s_haskey[tap]) {  // identity tap: R = (C0_c, D_{c,l}) in limb l
-        pr[t].c0 = __ldg(C0 + j);
-        pr[t].d[0] = __ldg(D + (size_t)l * LN + j);
-      } else {
-        const int jp = galois_perm(j, s_act[tap], N >> 1);
-        pr[t].c0 = __ldg(C0 + jp);
-#pragma unroll
-        for (int i = 0; i < LT; i++) pr[t].d[i] = __ldg(D + (size_t)i * LN + jp);
-      }
-    }
-  };
   const uint32_t idesc = umma_idesc_s8u8(128, 8 * TC_COLS);  // one UMMA covers the 8 byte planes
   // one register buffer (occupancy first: 2 CTAs x 12 warps per SM): the next chunk's digit
   // reads are issued right after this chunk's key switching
   Term* cur = pre;
-  load_chunk(0, pre);
 #pragma unroll 1
   for (int ch = 0; ch < nchunks; ch++) {
     const int s = ch % KT_STAGES;
@@ -1447,7 +1463,7 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   for (int ch = nchunks > KT_STAGES ? nchunks - KT_STAGES : 0; ch < nchunks; ch++)
     mbar_wait(&empty_bar[ch % KT_STAGES], (ch / KT_STAGES) & 1);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (warp < 8) {
+  if (warp < 8 && rows_live) {
     const int comp = chalf;
     const int row = mt * 128 + quad * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
@@ -1469,7 +1485,7 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
 #pragma unroll
         for (int b = 4; b < 8; b++) hi += (long long)(int32_t)v[b][cc] << (8 * (b - 4));
         const int col = c0 + cc;
-        tc_store(a, z, row, col >> 4, l, j0 + (col & 15), hi, lo);
+        tc_store<LT, LOGN>(a, z, row, col >> 4, l, j0 + (col & 15), hi, lo);
       }
     }
   }
@@ -1478,19 +1494,26 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS));
 }
 
-template <int LT>
-hy_status launch_ksmac_tc(const KsMacArgs& a, const int8_t* w8, int units, cudaStream_t s) {
+template <int LT, int LOGN>
+hy_status launch_ksmac_tc_t(const KsMacArgs& a, const int8_t* w8, int units, cudaStream_t s) {
   const int N = 1 << a.logN;
   static bool attr_done = false;
   if (!attr_done) {
-    HY_CUDA_TRY(cudaFuncSetAttribute(ksmac_tc_kernel<LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    HY_CUDA_TRY(cudaFuncSetAttribute(ksmac_tc_kernel<LT, LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kt_smem(HY_MAX_TAPS, LT)));
     attr_done = true;
   }
   dim3 grid((unsigned)(a.L * (N / TC_POS)), (unsigned)((a.Mpad + 127) / 128), (unsigned)units);
-  ksmac_tc_kernel<LT><<<grid, KT_THREADS, kt_smem(a.T, LT), s>>>(a, w8);
+  ksmac_tc_kernel<LT, LOGN><<<grid, KT_THREADS, kt_smem(a.T, LT), s>>>(a, w8);
   HY_LAUNCH_CHECK();
   return HY_OK;
+}
+
+// N = 8192 (the metric's ring degree) gets compile-time address math; other N the generic kernel
+template <int LT>
+hy_status launch_ksmac_tc(const KsMacArgs& a, const int8_t* w8, int units, cudaStream_t s) {
+  if (a.logN == 13) return launch_ksmac_tc_t<LT, 13>(a, w8, units, s);
+  return launch_ksmac_tc_t<LT, 0>(a, w8, units, s);
 }
 
 hy_status launch_mac_tc(const KsMacArgs& a, const u64* R, const int8_t* w8, int units, cudaStream_t s) {

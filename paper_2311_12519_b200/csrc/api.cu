@@ -435,7 +435,7 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
     w->K = (int)lay.Jc * T;
     w->wblocks = 1;
   }
-  w->Mpad = hy_mac_mpad(w->M);
+  w->Mpad = hy_mac_mpad(w->M, dw);
   w->mac_path = hy_mac_path(w->M, (int)p->L, dw, coef_ok(w, lay));
   w->Kpad = (w->K + 31) / 32 * 32;  // multiple of the MAC K chunks (16 FP64 GEMM, 32 tcgen05)
   // weight table (S0), [block][kk][row] as exact doubles; row semantics documented in DESIGN.md §4

@@ -106,15 +106,15 @@ bool hy_galois_act(uint32_t g, uint32_t N, GaloisAct* out);
 
 // Row tile of the fused S2+S3 kernel for M MAC rows: -MR = thin kernel with MR <= 2 rows,
 // else WM warps (8 rows each).  Shared by hy_encode_weights (table padding) and the launcher.
-inline int hy_mac_tile(int M) {
-  if (M <= 2) return -M;
+inline int hy_mac_tile(int M, bool depthwise) {
+  if (depthwise) return -M;  // M <= 2: thin kernel (one term per tap, one input ct per unit)
   if (M <= 8) return 1;
   if (M <= 16) return 2;
   if (M <= 32) return 4;
   return 8;
 }
-inline int hy_mac_mpad(int M) {
-  const int t = hy_mac_tile(M);
+inline int hy_mac_mpad(int M, bool depthwise) {
+  const int t = hy_mac_tile(M, depthwise);
   const int bm = t < 0 ? -t : 8 * t;
   return (M + bm - 1) / bm * bm;
 }  // false if g is not odd / not in Z_2N^*

@@ -387,6 +387,7 @@ struct KsMacArgs {
     GaloisAct act[HY_MAX_TAPS];
   } tt;
   int T, Jcb, K, Kpad, M, Mpad, wblocks, L, logN, kscale, cn;
+  int dbg;                     // measurement experiments only (HY_DEBUG_KSMAC): 1 = skip the UMMAs
   LimbConsts lcs;
 };
 
@@ -759,39 +760,98 @@ __global__ void __launch_bounds__(256, 2) ksmac_gemm_kernel(KsMacArgs a) {
   }
 }
 
-// ---- thin variant (M <= 2 rows: depthwise): one thread per (limb, position), all K terms in
-// registers, no shared memory.
-template <int MR, int LT>
-__global__ void __launch_bounds__(256) ksmac_thin_kernel(KsMacArgs a) {
+// ---- thin variant (M <= 2 rows: depthwise): one thread per (limb, position) and CPT units
+// (input cts with their own weight block), all K = T taps in registers, no shared memory.  The
+// tap's key words are loaded once per tap and reused for the CPT units (the key traffic, 4L words
+// per (ct, tap) before, dominated the loads); digit reads are issued for all CPT units before the
+// key switching of the first.
+template <int MR, int LT, int CPT>
+__global__ void __launch_bounds__(256) ksmac_thin_kernel(KsMacArgs a, int units) {
   const int N = 1 << a.logN;
   const int idx = blockIdx.x * 256 + threadIdx.x;
   const int l = idx >> a.logN, j = idx & (N - 1);
   if (l >= a.L) return;
-  const int z = blockIdx.z;
-  const double* __restrict__ wt = a.wt + (size_t)(z % a.wblocks) * a.Kpad * a.Mpad;
+  const int z0 = blockIdx.z * CPT;
   const LimbConst cst = a.lcs.lc[l];
-  double ah[2][MR], al[2][MR];
+  double ah[CPT][2][MR], al[CPT][2][MR];
 #pragma unroll
-  for (int c = 0; c < 2; c++)
+  for (int u = 0; u < CPT; u++)
 #pragma unroll
-    for (int r = 0; r < MR; r++) ah[c][r] = al[c][r] = 0.0;
-  KeyRegs<LT> kr;
-  for (int kk = 0; kk < a.K; kk++) {
-    u64 r0, r1;
-    r_value<LT>(a, a.keys, a.act, z, kk, l, j, cst, kr, r0, r1);
-    const double x0h = (double)(uint32_t)(r0 >> 30), x0l = (double)(uint32_t)(r0 & M30);
-    const double x1h = (double)(uint32_t)(r1 >> 30), x1l = (double)(uint32_t)(r1 & M30);
+    for (int c = 0; c < 2; c++)
 #pragma unroll
-    for (int r = 0; r < MR; r++) {
-      const double w = __ldg(wt + (size_t)kk * a.Mpad + r);
-      ah[0][r] = fma(w, x0h, ah[0][r]);
-      al[0][r] = fma(w, x0l, al[0][r]);
-      ah[1][r] = fma(w, x1h, ah[1][r]);
-      al[1][r] = fma(w, x1l, al[1][r]);
+      for (int r = 0; r < MR; r++) ah[u][c][r] = al[u][c][r] = 0.0;
+  const size_t LN = (size_t)(LT > 0 ? LT : a.L) * N;
+  for (int kk = 0; kk < a.K; kk++) {  // depthwise: one term per tap
+    const u64* key = a.tt.key[kk];
+    KeyRegs<LT> kr;
+    int jp = j;
+    if (key != nullptr) {
+      jp = galois_perm(j, a.tt.act[kk], N >> 1);
+      if constexpr (LT > 0) kr.load(key, a.logN, l, j);
+    }
+    u64 c0v[CPT], dv[CPT][LT > 0 ? LT : 1];
+#pragma unroll
+    for (int u = 0; u < CPT; u++) {
+      const int z = z0 + u < units ? z0 + u : units - 1;  // clamp: the tail's extra work is discarded
+      const u64* C0 = a.C0 + (size_t)z * LN;
+      const u64* D = a.D + (size_t)z * (LT > 0 ? LT : a.L) * LN;
+      c0v[u] = __ldg(C0 + (size_t)l * N + jp);
+      if constexpr (LT > 0) {
+        if (key == nullptr) {
+          dv[u][0] = __ldg(D + ((size_t)l * LT + l) * N + jp);
+        } else {
+#pragma unroll
+          for (int i = 0; i < LT; i++) dv[u][i] = __ldg(D + ((size_t)i * LT + l) * N + jp);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < CPT; u++) {
+      const int z = z0 + u < units ? z0 + u : units - 1;
+      u64 r0, r1;
+      if constexpr (LT > 0) {
+        if (key == nullptr) {
+          r0 = c0v[u];
+          r1 = dv[u][0];
+        } else {
+          const u64 q = cst.q, q2 = cst.two_q;
+          u64 x0 = c0v[u], x1 = 0;
+#pragma unroll
+          for (int i = 0; i < LT; i++) {
+            x0 = csub(x0 + shoup_mul(dv[u][i], kr.v[2 * i], kr.sh[2 * i], q), q2);
+            x1 = csub(x1 + shoup_mul(dv[u][i], kr.v[2 * i + 1], kr.sh[2 * i + 1], q), q2);
+          }
+          r0 = csub(x0, q);  // canonical: the 30-bit split needs R < 2^60
+          r1 = csub(x1, q);
+        }
+      } else {
+        const u64* C0 = a.C0 + (size_t)z * LN;
+        const u64* D = a.D + (size_t)z * a.L * LN;
+        if (key == nullptr) {
+          r0 = c0v[u];
+          r1 = __ldg(D + ((size_t)l * a.L + l) * N + j);
+        } else {
+          ks_pair_any(D, C0, key, a.L, a.logN, l, j, jp, cst, r0, r1);
+        }
+      }
+      const double x0h = (double)(uint32_t)(r0 >> 30), x0l = (double)(uint32_t)(r0 & M30);
+      const double x1h = (double)(uint32_t)(r1 >> 30), x1l = (double)(uint32_t)(r1 & M30);
+      const double* __restrict__ wt = a.wt + (size_t)(z % a.wblocks) * a.Kpad * a.Mpad;
+#pragma unroll
+      for (int r = 0; r < MR; r++) {
+        const double w = __ldg(wt + (size_t)kk * a.Mpad + r);
+        ah[u][0][r] = fma(w, x0h, ah[u][0][r]);
+        al[u][0][r] = fma(w, x0l, al[u][0][r]);
+        ah[u][1][r] = fma(w, x1h, ah[u][1][r]);
+        al[u][1][r] = fma(w, x1l, al[u][1][r]);
+      }
     }
   }
 #pragma unroll
-  for (int c = 0; c < 2; c++) store_outputs(a, z, 0, c, l, j, ah[c], al[c], MR);
+  for (int u = 0; u < CPT; u++)
+    if (z0 + u < units)
+#pragma unroll
+      for (int c = 0; c < 2; c++) store_outputs(a, z0 + u, 0, c, l, j, ah[u][c], al[u][c], MR);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1245,7 +1305,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mac_tc_kernel(KsMacArgs a, cons
 // its 2 x 8 UMMAs (M = 128, N = 32, K = 32, s8 x u8 -> s32) into the 8 TMEM accumulators.  TMEM is
 // zeroed first and every UMMA accumulates: integer sums are exact, so the issue order of chunks by
 // different warps does not matter.
-constexpr int KT_THREADS = 384, KT_WARPS = KT_THREADS / 32, KT_STAGES = 2, KT_KS = 3, KT_CHUNK = 32 * KT_KS;
+constexpr int KT_THREADS = 256, KT_WARPS = KT_THREADS / 32, KT_STAGES = 3, KT_KS = 2, KT_CHUNK = 32 * KT_KS;
 constexpr int KT_STAGE_A = KT_KS * 4096, KT_STAGE_B = KT_KS * 8 * 1024;
 constexpr size_t KT_SMEM_MMA = (size_t)KT_STAGES * (KT_STAGE_A + KT_STAGE_B) + 1024;
 inline size_t kt_smem(int T, int L) { return KT_SMEM_MMA + (size_t)T * 4 * L * TC_POS * sizeof(u64); }
@@ -1313,7 +1373,11 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
       pr[t].tap = tap;
       const u64* C0 = C0u + (size_t)c * LN;
       const u64* D = Du + (size_t)c * (LT * LN);
-      if (a.tt.key[tap] == nullptr) {  // identity tap: R = (C0_c, D_{c,l}) in limb l
+      if (a.dbg & 4) {
+        pr[t].c0 = c;
+#pragma unroll
+        for (int i = 0; i < LT; i++) pr[t].d[i] = c + i;
+      } else if (a.tt.key[tap] == nullptr) {  // identity tap: R = (C0_c, D_{c,l}) in limb l
         pr[t].c0 = __ldg(C0 + j);
         pr[t].d[0] = __ldg(D + l * LN + j);
       } else {
@@ -1337,7 +1401,7 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
     s_act[t] = a.tt.act[t];
   }
   // stage the key words of this CTA (limb l, positions j0 .. j0 + 15) for every tap
-  for (int e = tid; e < a.T * 4 * LT * TC_POS; e += KT_THREADS) {
+  for (int e = tid; e < ((a.dbg & 16) ? 0 : a.T * 4 * LT * TC_POS); e += KT_THREADS) {
     const int p = e % TC_POS, r = e / TC_POS;
     const int sh = r % 2, x = (r / 2) % (2 * LT), tap = r / (4 * LT);
     const u64* key = a.tt.key[tap];
@@ -1399,7 +1463,7 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
       u64 r0 = 0, r1 = 0;
       if (tap >= 0) {
         r0 = cur[t].c0;
-        if (!s_haskey[tap]) {
+        if (!s_haskey[tap] || (a.dbg & 2)) {
           r1 = cur[t].d[0];
         } else {
           const u64* kp = skey + (size_t)tap * 4 * LT * TC_POS + pos;
@@ -1441,7 +1505,7 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
       if (prev % KT_WARPS == KT_WARPS - 1) {       // 8u .. 8u + 7; the last warp issues the UMMAs
         __threadfence_block();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        for (int k2 = 0; k2 < KT_KS && KT_KS * ch + k2 < nk32; k2++) {
+        for (int k2 = 0; k2 < KT_KS && KT_KS * ch + k2 < nk32 && !(a.dbg & 1); k2++) {
           const uint64_t da = umma_desc_kmajor(smem_u32(sA(s, k2)));
           const uint64_t db = umma_desc_kmajor(smem_u32(sB(s, k2, 0)));  // all 8 planes: N = 256
           asm volatile(
@@ -1463,7 +1527,7 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   for (int ch = nchunks > KT_STAGES ? nchunks - KT_STAGES : 0; ch < nchunks; ch++)
     mbar_wait(&empty_bar[ch % KT_STAGES], (ch / KT_STAGES) & 1);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (warp < 8 && rows_live) {
+  if (warp < 8 && rows_live && !(a.dbg & 8)) {
     const int comp = chalf;
     const int row = mt * 128 + quad * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
@@ -1576,8 +1640,9 @@ hy_status launch_ksmac_gemm(const KsMacArgs& a, int units, cudaStream_t s) {
 template <int MR, int LT>
 hy_status launch_ksmac_thin(const KsMacArgs& a, int units, cudaStream_t s) {
   const int N = 1 << a.logN;
-  dim3 grid((unsigned)((a.L * N + 255) / 256), 1, (unsigned)units);
-  ksmac_thin_kernel<MR, LT><<<grid, 256, 0, s>>>(a);
+  constexpr int CPT = LT == 5 ? 2 : 4;  // units per thread (registers: CPT x (L + 1) digits + 4 MR sums)
+  dim3 grid((unsigned)((a.L * N + 255) / 256), 1, (unsigned)((units + CPT - 1) / CPT));
+  ksmac_thin_kernel<MR, LT, CPT><<<grid, 256, 0, s>>>(a, units);
   HY_LAUNCH_CHECK();
   return HY_OK;
 }
@@ -1671,6 +1736,8 @@ hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
   a.out = w->d_P;
   a.sign = w->d_sign;
   a.kt = w->d_kt;
+  static const int dbg = getenv("HY_DEBUG_KSMAC") ? atoi(getenv("HY_DEBUG_KSMAC")) : 0;
+  a.dbg = dbg;
   a.T = (int)lay.n_taps;
   a.Jcb = dw ? 1 : (int)lay.Jc;
   a.K = w->K;
@@ -1684,7 +1751,7 @@ hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
   a.cn = (int)lay.cn;
   a.lcs = limb_consts(p);
   const int units = (int)(dw ? nunits * lay.Jc : nunits);
-  const int tile = hy_mac_tile(w->M);
+  const int tile = hy_mac_tile(w->M, dw);
   const int path = w->mac_path;
   if (path == HY_MAC_THIN || path == HY_MAC_FP64_FUSED) {  // key switching fused into the FP64 MAC
     HY_TRY(mac_mark(w, s));
@@ -1693,6 +1760,7 @@ hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
     switch (p->L) {  // compile-time digit count for the common L
       case 2: st = launch_ksmac<2>(a, tile, units, s); break;
       case 3: st = launch_ksmac<3>(a, tile, units, s); break;
+      case 5: st = launch_ksmac<5>(a, tile, units, s); break;
       default: st = launch_ksmac<0>(a, tile, units, s); break;
     }
     HY_TRY(st);

@@ -131,7 +131,10 @@ hy_status hy_conv_eval(hy_weights* w, const uint64_t* ct_in, size_t J, uint64_t*
                        void* cuda_stream);
 
 /* Same computation from/to HOST buffers (pinned or pageable): copies ct_in to the device,
- * evaluates, copies ct_out back, and synchronises the stream before returning. */
+ * evaluates, copies ct_out back, and returns when the outputs are in host memory.  Pipelined over
+ * batches of whole units (up to 8 batches) on two library-owned copy streams, so uploads and
+ * downloads overlap the evaluation (pinned buffers needed for the overlap).  J, Jout as for
+ * hy_conv_eval.  Errors: HY_ESHAPE, HY_ENOKEY, HY_ECUDA. */
 hy_status hy_conv_eval_host(hy_weights* w, const uint64_t* ct_in_host, size_t J, uint64_t* ct_out_host,
                             size_t Jout, void* cuda_stream);
 

@@ -633,6 +633,12 @@ extern "C" void hy_weights_destroy(hy_weights* w) {
   cudaFree(w->d_R);
   cudaFree(w->d_in);
   cudaFree(w->d_out);
+  if (w->s_h2d) {
+    cudaStreamDestroy(w->s_h2d);
+    cudaStreamDestroy(w->s_d2h);
+    cudaEventDestroy(w->ev_h2d);
+    cudaEventDestroy(w->ev_comp);
+  }
   cudaFree(w->d_tap_keys);
   cudaFree(w->d_tap_act);
   if (w->mac_ev) {
@@ -714,14 +720,36 @@ extern "C" hy_status hy_conv_eval(hy_weights* w, const uint64_t* ct_in, size_t J
 extern "C" hy_status hy_conv_eval_host(hy_weights* w, const uint64_t* in, size_t J, uint64_t* out, size_t Jout,
                                        void* stream) {
   HY_CHECK(w && in && out, HY_EINVAL, "null argument");
+  const hy_layout& lay = w->lay;
   const size_t ctw = 2 * (size_t)w->p->L * w->p->N;
-  HY_CHECK(J <= (size_t)w->lay.U * w->lay.Jc && Jout <= (size_t)w->lay.U * w->lay.Jo, HY_ESHAPE, "too many cts");
+  HY_CHECK(J > 0 && J % lay.Jc == 0, HY_ESHAPE, "J=%zu is not a positive multiple of Jc=%u", J, lay.Jc);
+  const size_t nu = J / lay.Jc;
+  HY_CHECK(nu <= lay.U && Jout == nu * lay.Jo, HY_ESHAPE, "J=%zu / Jout=%zu do not match the layout", J, Jout);
   HY_CUDA_TRY(cudaSetDevice(w->p->device));
   cudaStream_t s = (cudaStream_t)stream;
-  HY_CUDA_TRY(cudaMemcpyAsync(w->d_in, in, J * ctw * sizeof(u64), cudaMemcpyHostToDevice, s));
-  HY_TRY(hy_conv_eval(w, w->d_in, J, w->d_out, Jout, stream));
-  HY_CUDA_TRY(cudaMemcpyAsync(out, w->d_out, Jout * ctw * sizeof(u64), cudaMemcpyDeviceToHost, s));
-  HY_CUDA_TRY(cudaStreamSynchronize(s));
+  if (!w->s_h2d) {
+    HY_CUDA_TRY(cudaStreamCreateWithFlags(&w->s_h2d, cudaStreamNonBlocking));
+    HY_CUDA_TRY(cudaStreamCreateWithFlags(&w->s_d2h, cudaStreamNonBlocking));
+    HY_CUDA_TRY(cudaEventCreateWithFlags(&w->ev_h2d, cudaEventDisableTiming));
+    HY_CUDA_TRY(cudaEventCreateWithFlags(&w->ev_comp, cudaEventDisableTiming));
+  }
+  // Pipelined over batches of units (units are independent): the upload of batch
+  // b + 1 and the download of batch b - 1 overlap the evaluation of batch b on the caller's stream.
+  const size_t nb = nu >= 8 ? (nu + 7) / 8 : nu;  // units per batch: 8 batches when possible
+  for (size_t u0 = 0; u0 < nu; u0 += nb) {
+    const size_t n = std::min(nb, nu - u0);
+    const size_t i0 = u0 * lay.Jc, ni = n * lay.Jc, o0 = u0 * lay.Jo, no = n * lay.Jo;
+    HY_CUDA_TRY(cudaMemcpyAsync(w->d_in + i0 * ctw, in + i0 * ctw, ni * ctw * sizeof(u64), cudaMemcpyHostToDevice,
+                                w->s_h2d));
+    HY_CUDA_TRY(cudaEventRecord(w->ev_h2d, w->s_h2d));
+    HY_CUDA_TRY(cudaStreamWaitEvent(s, w->ev_h2d, 0));
+    HY_TRY(hy_conv_eval(w, w->d_in + i0 * ctw, ni, w->d_out + o0 * ctw, no, stream));
+    HY_CUDA_TRY(cudaEventRecord(w->ev_comp, s));
+    HY_CUDA_TRY(cudaStreamWaitEvent(w->s_d2h, w->ev_comp, 0));
+    HY_CUDA_TRY(cudaMemcpyAsync(out + o0 * ctw, w->d_out + o0 * ctw, no * ctw * sizeof(u64), cudaMemcpyDeviceToHost,
+                                w->s_d2h));
+  }
+  HY_CUDA_TRY(cudaStreamSynchronize(w->s_d2h));
   return HY_OK;
 }
 

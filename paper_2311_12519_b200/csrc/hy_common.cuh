@@ -153,6 +153,8 @@ struct hy_weights {
   u64* d_X;         // [U*Jo][2][L][N] aligned outputs (NTT form) before the final INTT
   u64* d_R;         // [r_units][K][2][L][N] rotated inputs of the dense path (slot-order NTT)
   int r_units;      // units per PermAuto + MAC batch
+  cudaStream_t s_h2d, s_d2h;   // hy_conv_eval_host copy streams (created on first use)
+  cudaEvent_t ev_h2d, ev_comp;
   u64* d_in;        // staging for hy_conv_eval_host
   u64* d_out;
   u64** d_tap_keys;            // device array of key pointers per tap (nullptr = identity)

@@ -686,9 +686,10 @@ static hy_status bind_keys(hy_weights* w) {
 // ============================================================================================
 extern "C" hy_status hy_conv_eval(hy_weights* w, const uint64_t* ct_in, size_t J, uint64_t* ct_out, size_t Jout,
                                   void* stream) {
-  HY_CHECK(w && ct_in && ct_out, HY_EINVAL, "null argument");
+  HY_CHECK(w, HY_EINVAL, "null weights");
   const hy_layout& lay = w->lay;
   HY_CHECK(J > 0 && J % lay.Jc == 0, HY_ESHAPE, "J=%zu is not a positive multiple of Jc=%u", J, lay.Jc);
+  HY_CHECK(ct_in && ct_out, HY_EINVAL, "null argument");
   const size_t nu = J / lay.Jc;
   HY_CHECK(nu <= lay.U, HY_ESHAPE, "J=%zu covers %zu units > U=%u", J, nu, lay.U);
   HY_CHECK(Jout == nu * lay.Jo, HY_ESHAPE, "Jout=%zu, expected %zu", Jout, nu * lay.Jo);
@@ -719,10 +720,11 @@ extern "C" hy_status hy_conv_eval(hy_weights* w, const uint64_t* ct_in, size_t J
 
 extern "C" hy_status hy_conv_eval_host(hy_weights* w, const uint64_t* in, size_t J, uint64_t* out, size_t Jout,
                                        void* stream) {
-  HY_CHECK(w && in && out, HY_EINVAL, "null argument");
+  HY_CHECK(w, HY_EINVAL, "null weights");
   const hy_layout& lay = w->lay;
   const size_t ctw = 2 * (size_t)w->p->L * w->p->N;
   HY_CHECK(J > 0 && J % lay.Jc == 0, HY_ESHAPE, "J=%zu is not a positive multiple of Jc=%u", J, lay.Jc);
+  HY_CHECK(in && out, HY_EINVAL, "null argument");
   const size_t nu = J / lay.Jc;
   HY_CHECK(nu <= lay.U && Jout == nu * lay.Jo, HY_ESHAPE, "J=%zu / Jout=%zu do not match the layout", J, Jout);
   HY_CUDA_TRY(cudaSetDevice(w->p->device));

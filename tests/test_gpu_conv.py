@@ -95,6 +95,11 @@ CASES = {
                    xrange=(-128, 128), wrange=(-128, 128)),
     "tc_cn2_L5_rows130": dict(N=1024, bits=50, L=5, batch=2, Ci=2, Co=65, H=5, W=5, kh=3, kw=3, pad=1),
     "tc_pw_cn1": dict(N=1024, bits=50, L=3, batch=9, Ci=40, Co=66, H=6, W=6, kh=1, kw=1, pad=0),
+    # degenerate layers: one channel of one pixel (c_n = 2 with an empty second slot row), a 1x1
+    # single-channel layer, the largest kernel (7x7 = HY_MAX_TAPS taps) on a 3x3 image
+    "one_pixel": dict(N=1024, bits=50, L=2, batch=1, Ci=1, Co=1, H=1, W=1, kh=3, kw=3, pad=1),
+    "pw_one_channel": dict(N=1024, bits=50, L=2, batch=3, Ci=1, Co=1, H=5, W=5, kh=1, kw=1, pad=0),
+    "k7x7": dict(N=1024, bits=50, L=2, batch=1, Ci=2, Co=3, H=3, W=3, kh=7, kw=7, pad=3),
     # K = Jc * 9 = 297 terms: 5 chunks of 64 with a ragged last K step; 128 rows exactly
     "tc_cn2_k297_rows128": dict(N=1024, bits=60, L=3, batch=1, Ci=66, Co=64, H=5, W=5, kh=3, kw=3, pad=1,
                                 xrange=(-128, 128), wrange=(-128, 128)),
@@ -154,6 +159,36 @@ def test_shape_errors(hy):
             x2 = torch.zeros((2, 2, L, N), dtype=torch.uint64, device="cuda")
             with pytest.raises(hy.HyenaError, match="no Galois key"):
                 hy.hy_conv_eval(w, x2, x2)
+        finally:
+            hy.hy_weights_destroy(w)
+    finally:
+        hy.hy_params_destroy(p)
+
+
+def test_empty_and_misaligned_inputs(hy):
+    """J = 0 and J not a multiple of Jc are rejected by both entry points, with no launch."""
+    c = dict(CASES["cn1_blocks_tail"])
+    N, bits, L = c.pop("N"), c.pop("bits"), c.pop("L")
+    lay = make_layer(N, ntt_primes(N, bits, L), seed=570, **c)
+    p = hy.hy_params_create(N, lay.P.primes, 65537)
+    try:
+        elts = list(lay.keys)
+        hy.hy_keys_upload(p, elts, np.stack([lay.keys[g] for g in elts]))
+        w = hy.hy_encode_weights(p, lay.W, **shape_of(lay))
+        try:
+            Lay = hy.hy_weights_layout(w)
+            n0 = hy.hy_kernel_launches()
+            x = torch.zeros((0, 2, L, N), dtype=torch.uint64, device="cuda")
+            with pytest.raises(hy.HyenaError, match="positive multiple"):
+                hy.hy_conv_eval(w, x, x)
+            h = np.zeros((0, 2, L, N), dtype=np.uint64)
+            with pytest.raises(hy.HyenaError, match="positive multiple"):
+                hy.hy_conv_eval_host(w, h, h)
+            if Lay.Jc > 1:
+                h1 = np.zeros((Lay.Jc + 1, 2, L, N), dtype=np.uint64)
+                with pytest.raises(hy.HyenaError, match="multiple of Jc"):
+                    hy.hy_conv_eval_host(w, h1, np.zeros((Lay.Jo, 2, L, N), dtype=np.uint64))
+            assert hy.hy_kernel_launches() == n0
         finally:
             hy.hy_weights_destroy(w)
     finally:

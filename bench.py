@@ -295,10 +295,16 @@ def roofline(cfg, res, peaks, steps):
     per_step = max(1, res["mac_launches"] // max(1, steps))
     dom = max(st, key=st.get)
     kernels = {}
+    if path == "tc_coef":           # 1x1 coefficient-domain MAC: no S1; c_n = 2 keeps the row swap
+        L, N = len(cfg.primes), cfg.N
+        bfly = N // 2 * int(np.log2(N))
+        w["modmul"]["S1_permdecomp"] = 0
+        w["modmul"]["S4S5_align_intt"] = (lay.Jout * ((L * L + L) * bfly + 2 * L * L * N + 2 * L * bfly)
+                                          if lay.cn == 2 else 0)
     for stage in ("S1_permdecomp", "S4S5_align_intt"):
-        if path == "tc_coef":       # 1x1 coefficient-domain MAC: no NTT stages at all
+        if w["modmul"][stage] == 0:   # empty stage (1x1 coefficient-domain path)
             kernels[stage] = {"bound": "none", "achieved": 0.0, "peak": int_peak, "unit": "Gmodmul/s", "frac": 0.0,
-                              "ms": st[stage], "note": "empty stage (no NTT in the 1x1 c_n = 1 path)"}
+                              "ms": st[stage], "note": "empty stage (no NTT in this stage of the 1x1 path)"}
             continue
         a = w["modmul"][stage] / (st[stage] * 1e-3) / 1e9 if st[stage] > 0 else 0.0
         kernels[stage] = {"bound": "alu", "achieved": a, "peak": int_peak, "unit": "Gmodmul/s",

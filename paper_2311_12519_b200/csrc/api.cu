@@ -408,9 +408,9 @@ extern "C" hy_status hy_keys_upload(hy_params* p, uint32_t n, const uint32_t* el
 // ============================================================================================
 // weights
 // ============================================================================================
-// 1x1 kernel, no padding, c_n = 1, dense: the coefficient-domain MAC applies (HY_MAC_TC_COEF)
+// 1x1 kernel, no padding, dense: the coefficient-domain MAC applies (HY_MAC_TC_COEF)
 static bool coef_ok(const hy_weights* w, const hy_layout& lay) {
-  return !w->shape.depthwise && lay.n_taps == 1 && lay.tap_step[0] == 0 && lay.cn == 1;
+  return !w->shape.depthwise && lay.n_taps == 1 && lay.tap_step[0] == 0;
 }
 
 extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, const int8_t* Wt, hy_weights** out) {
@@ -527,11 +527,12 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
     u64** ptr;
     size_t words;
   } allocs[] = {
-      {&w->d_D, Jin * L * L * N},
-      {&w->d_C0, Jin * L * N},
+      {&w->d_D, std::max(Jin, (lay.cn == 2 && w->mac_path == HY_MAC_TC_COEF) ? Jo : 0) * L * L * N},
+      {&w->d_C0, std::max(Jin, (lay.cn == 2 && w->mac_path == HY_MAC_TC_COEF) ? Jo : 0) * L * N},
       {&w->d_P, Jo * ctw * ((lay.cn == 2 && !dw) ? 2 : 1)},
       {&w->d_D2, (lay.cn == 2 && !dw) ? Jo * L * L * N + Jo * L * N : 0},
       {&w->d_X, (lay.cn == 2 && !dw) ? Jo * ctw : 0},
+      {&w->d_A1, (lay.cn == 2 && w->mac_path == HY_MAC_TC_COEF) ? Jo * 2 * ctw : 0},
       {&w->d_R, (w->mac_path == HY_MAC_TC_SPLIT || w->mac_path == HY_MAC_FP64_SPLIT)
                     ? (size_t)w->r_units * w->K * ctw : 0},
       {&w->d_in, Jin * ctw},
@@ -598,6 +599,25 @@ extern "C" hy_status hy_weights_set_mac_path(hy_weights* w, int32_t path) {
   HY_CHECK(ok, HY_EINVAL, "MAC path %d is not valid for this layout (M = %d, L = %d, depthwise = %d)", path, w->M, L,
            (int)dw);
   cudaSetDevice(w->p->device);
+  if (path == HY_MAC_TC_COEF && w->lay.cn == 2) {  // [A1] buffer and Jo-sized digit workspaces
+    const size_t N = w->p->N, ctw = 2 * (size_t)L * N, Jin = (size_t)w->lay.U * w->lay.Jc,
+                 Jo = (size_t)w->lay.U * w->lay.Jo;
+    if (!w->d_A1 && cudaMalloc(&w->d_A1, Jo * 2 * ctw * sizeof(u64)) != cudaSuccess) {
+      w->d_A1 = nullptr;
+      hy_set_error("coefficient-domain workspace allocation failed");
+      return HY_ENOMEM;
+    }
+    if (Jo > Jin) {
+      cudaFree(w->d_D);
+      cudaFree(w->d_C0);
+      w->d_D = w->d_C0 = nullptr;
+      if (cudaMalloc(&w->d_D, Jo * L * L * N * sizeof(u64)) != cudaSuccess ||
+          cudaMalloc(&w->d_C0, Jo * L * N * sizeof(u64)) != cudaSuccess) {
+        hy_set_error("coefficient-domain digit workspace allocation failed");
+        return HY_ENOMEM;
+      }
+    }
+  }
   const bool split = path == HY_MAC_TC_SPLIT || path == HY_MAC_FP64_SPLIT;
   if (split && !w->d_R) {
     const size_t words = (size_t)w->r_units * w->K * 2 * L * w->p->N;
@@ -630,6 +650,7 @@ extern "C" void hy_weights_destroy(hy_weights* w) {
   cudaFree(w->d_P);
   cudaFree(w->d_D2);
   cudaFree(w->d_X);
+  cudaFree(w->d_A1);
   cudaFree(w->d_R);
   cudaFree(w->d_in);
   cudaFree(w->d_out);
@@ -706,6 +727,7 @@ extern "C" hy_status hy_conv_eval(hy_weights* w, const uint64_t* ct_in, size_t J
     HY_TRY(mark(1));
     HY_TRY(hyk::mac_coef(w, ct_in, nu, ct_out, s));
     HY_TRY(mark(2));
+    if (lay.cn == 2) HY_TRY(hyk::finish_coef2(w, nu, ct_out, s));  // sign PMult + row swap
     HY_TRY(mark(3));
     return HY_OK;
   }

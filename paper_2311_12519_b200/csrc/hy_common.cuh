@@ -126,7 +126,8 @@ enum HyMacPath {
   HY_MAC_TC_SPLIT = 2,    // dense, M > 128: PermAuto materialises R, tcgen05 MAC consumes it
   HY_MAC_FP64_FUSED = 3,  // A/B option HY_MAC_FP64 (M <= 32): key switching + FP64 DFMA MAC
   HY_MAC_FP64_SPLIT = 4,  // A/B option HY_MAC_FP64 (M > 32): PermAuto + FP64 DFMA MAC
-  HY_MAC_TC_COEF = 5,     // 1x1, c_n = 1: tcgen05 MAC straight on the coefficient-form inputs, no NTT
+  HY_MAC_TC_COEF = 5,     // 1x1: tcgen05 MAC straight on the coefficient-form inputs (c_n = 1: no NTT;
+                          // c_n = 2: only the row-swap alignment's NTTs)
 };
 int hy_mac_path(int M, int L, bool depthwise, bool coef_ok);
 
@@ -151,6 +152,7 @@ struct hy_weights {
   u64* d_P;         // [U*Jo][cn'][2][L][N] partial sums (NTT form)
   u64* d_D2;        // [U*Jo][L][L][N] digits of P_{g,1}.c1 for the row swap
   u64* d_X;         // [U*Jo][2][L][N] aligned outputs (NTT form) before the final INTT
+  u64* d_A1;        // [U*Jo][2][2][L][N] [A1] of the coefficient-domain c_n = 2 1x1 path
   u64* d_R;         // [r_units][K][2][L][N] rotated inputs of the dense path (slot-order NTT)
   int r_units;      // units per PermAuto + MAC batch
   cudaStream_t s_h2d, s_d2h;   // hy_conv_eval_host copy streams (created on first use)
@@ -215,6 +217,7 @@ hy_status permdecomp(const hy_params* p, const u64* ct, size_t nct, u64* D, u64*
 hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s);  // S2 + S3
 hy_status finish_outputs(const hy_weights* w, size_t nunits, u64* ct_out, cudaStream_t s);
 hy_status mac_coef(hy_weights* w, const u64* ct_in, size_t nunits, u64* ct_out, cudaStream_t s);
+hy_status finish_coef2(const hy_weights* w, size_t nunits, u64* ct_out, cudaStream_t s);
 hy_status rotate_ct(const hy_params* p, const u64* ct_in, GaloisAct act, const u64* key, u64* ct_out, size_t n,
                     u64* work, cudaStream_t s);
 hy_status decrypt_phase(const hy_params* p, const u64* s_ntt, const u64* s_ntt_sh, const u64* ct, size_t n,

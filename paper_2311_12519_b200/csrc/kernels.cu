@@ -52,6 +52,7 @@ struct PermDecompJob {
   u64* C0;
   int L, N;
   QArr qa;
+  size_t ct_stride;  // words between consecutive input cts (0 = 2 L N, contiguous)
   int limb;
   const u64* s;
   u64* d;
@@ -60,16 +61,17 @@ struct PermDecompJob {
   __device__ void bind(int b) {
     const int per = L * L + L;
     const int c = b / per, r = b % per;
+    const u64* cb = ct + (size_t)c * (ct_stride ? ct_stride : (size_t)2 * L * N);
     if (r < L * L) {
       const int i = r / L;
       limb = r % L;
-      s = ct + ((size_t)(2 * c + 1) * L + i) * N;
+      s = cb + ((size_t)L + i) * N;
       d = D + ((size_t)(c * L + i) * L + limb) * N;
       qd = qa.q[limb];
       red = qa.q[i] / 4 >= qa.q[limb];  // digit may exceed the lazy [0, 4 q_l) input range
     } else {
       limb = r - L * L;
-      s = ct + ((size_t)(2 * c) * L + limb) * N;
+      s = cb + (size_t)limb * N;
       d = C0 + ((size_t)c * L + limb) * N;
       qd = qa.q[limb];
       red = false;
@@ -218,6 +220,33 @@ struct OutInvJob {
   }
   __device__ u64 load(int k) const { return s[k]; }
   __device__ void store(int k, u64 v) const { d[k] = v; }
+};
+
+// INTT of X [o][2][L][N] plus a coefficient-form addend [o] at add + o * add_stride -> out
+// (the coefficient-domain row-swap alignment: Out = P_0 + INTT(KeySwitch(P_1)))
+struct OutInvAddJob {
+  const u64* X;
+  const u64* add;
+  size_t add_stride;
+  u64* out;
+  int L, N;
+  QArr qa;
+  int limb;
+  const u64* s;
+  const u64* ad;
+  u64* d;
+  u64 qd;
+  __device__ void bind(int b) {
+    const int o = b / (2 * L);
+    const int cl = b % (2 * L);
+    limb = cl % L;
+    qd = qa.q[limb];
+    s = X + ((size_t)o * 2 * L + cl) * N;
+    ad = add + (size_t)o * add_stride + (size_t)cl * N;
+    d = out + ((size_t)o * 2 * L + cl) * N;
+  }
+  __device__ u64 load(int k) const { return s[k]; }
+  __device__ void store(int k, u64 v) const { d[k] = csub(v + ad[k], qd); }
 };
 
 // c = INTT(A .* B) where A, B are NTT form [n][L][N] (slow generic product: debug paths only)
@@ -382,6 +411,7 @@ struct KsMacArgs {
   u64* out;                    // [z][M'][2][L][N], M' = M (cn 1) or M/2 (cn 2)
   const u64* sign;             // [L][N] sign plaintext (NTT), then [L][N] Shoup companions
   const int32_t* kt;           // fused tensor-core MAC: K term -> (tap << 16) | ct (-1 = padding)
+  u64* out2;                   // coefficient-domain c_n = 2 (tc_coef): [A1] here, [A0] in out; else null
   struct Taps {                // key pointers + automorphisms per tap, by value (no pointer chase)
     const u64* key[HY_MAX_TAPS];
     GaloisAct act[HY_MAX_TAPS];
@@ -1135,6 +1165,12 @@ __device__ __forceinline__ void tc_store(const KsMacArgs& a, int z, int row, int
   // Walsh-Hadamard on the exact accumulators (Eq. 2): A0 = k (B0 + B1), A1 = B0 - B1
   const u64 a0 = red(k * (H + H1), k * (Lo + L1));
   const u64 a1 = red(H - H1, Lo - L1);
+  if (a.out2) {  // coefficient domain: the sign PMult is a negacyclic shift, applied by sign_combine
+    const size_t at = ((size_t)(z * (a.M / 2) + row / 2) * 2 + comp) * LN + (size_t)l * N + j;
+    a.out[at] = a0;
+    a.out2[at] = a1;
+    return;
+  }
   const u64 sg = __ldg(a.sign + (size_t)l * N + j), sgs = __ldg(a.sign + LN + (size_t)l * N + j);
   u64 v = a0 + shoup_mul(a1, sg, sgs, c.q);
   v = csub(csub(v, c.two_q), c.q);
@@ -1723,7 +1759,7 @@ hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
   const hy_params* p = w->p;
   const hy_layout& lay = w->lay;
   const bool dw = w->shape.depthwise != 0;
-  KsMacArgs a;
+  KsMacArgs a{};
   a.D = w->d_D;
   a.C0 = w->d_C0;
   a.keys = w->d_tap_keys;
@@ -1807,6 +1843,25 @@ hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
   return HY_OK;
 }
 
+// P = [A0] + S * [A1] in the coefficient domain, S = s (X^{N/4} + X^{3N/4}) (the [k, -k] sign
+// plaintext): (S * A1)[j] = s (+/- A1[j - N/4] +/- A1[j - 3N/4]) with the
+// negacyclic sign for wrapped indices.  In place over P (= A0) [n][2][L][N]; canonical output.
+__global__ void sign_combine_kernel(u64* __restrict__ P, const u64* __restrict__ A1, size_t total, int logN, int L,
+                                    LimbConsts lcs, QArr sv, QArr svsh) {
+  const int N = 1 << logN;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i & (N - 1));
+    const int l = (int)((i >> logN) % L);
+    const u64 q = lcs.lc[l].q;
+    const size_t row = i - j;
+    const u64 t1 = A1[row + ((j - N / 4) & (N - 1))], t3 = A1[row + ((j - 3 * N / 4) & (N - 1))];
+    const u64 u = (j >= N / 4 ? t1 : q - t1) + (j >= 3 * N / 4 ? t3 : q - t3);  // < 2q
+    u64 v = P[i] + shoup_mul(u, sv.q[l], svsh.q[l], q);
+    v = csub(v, 2 * q);
+    P[i] = csub(v, q);
+  }
+}
+
 // 1x1 convolution with c_n = 1 (SURVEY §8(a) special case): the only tap is
 // the identity, so the hoisted rotation is the input itself and the MAC is linear: computing
 // Out_o = sum_c W[o][c] ct_c on the coefficient-form inputs and reducing once gives the same
@@ -1815,7 +1870,7 @@ hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
 hy_status mac_coef(hy_weights* w, const u64* ct_in, size_t nunits, u64* ct_out, cudaStream_t s) {
   w->mac_launches = 0;
   const hy_params* p = w->p;
-  KsMacArgs a;
+  KsMacArgs a{};
   a.out = ct_out;
   a.sign = nullptr;
   a.T = 1;
@@ -1827,15 +1882,61 @@ hy_status mac_coef(hy_weights* w, const u64* ct_in, size_t nunits, u64* ct_out, 
   a.wblocks = w->wblocks;
   a.L = (int)p->L;
   a.logN = (int)p->logN;
-  a.kscale = 1;
-  a.cn = 1;
+  a.kscale = (int)w->lay.k;
+  a.cn = (int)w->lay.cn;
   a.lcs = limb_consts(p);
+  a.out2 = nullptr;
+  if (a.cn == 2) {  // [A0] -> P, [A1] -> A1 buffer; the sign PMult and the row swap follow
+    a.out = w->d_P;
+    a.out2 = w->d_A1;
+  }
   HY_TRY(mac_mark(w, s));
   if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[0], s));
   HY_TRY(launch_mac_tc(a, ct_in, w->d_w8, (int)nunits, s));
   if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[1], s));
   w->mac_launches = 1;
   return HY_OK;
+}
+
+// c_n = 2 coefficient-domain 1x1 layer after mac_coef: P_d = [A0] + S * [A1]; Out_g = P_0 +
+// RowSwap(P_1) with RowSwap = the hoisted HRot by 2N - 1 (R15), whose digits are
+// the coefficient-form P_1.c1 limbs themselves (PermDecomp: L^2 + L NTTs per output ct).
+hy_status finish_coef2(const hy_weights* w, size_t nunits, u64* ct_out, cudaStream_t s) {
+  const hy_params* p = w->p;
+  const size_t L = p->L, N = p->N, ctw = 2 * L * N;
+  const size_t nout = nunits * w->lay.Jo;
+  QArr sv, svsh;
+  for (size_t l = 0; l < L; l++) {
+    const int64_t sc = w->lay.sign_coeff;
+    const u64 q = p->q[l];
+    sv.q[l] = sc >= 0 ? (u64)sc % q : q - ((u64)(-sc) % q);
+    svsh.q[l] = (u64)(((u128)sv.q[l] << 64) / q);
+  }
+  const size_t total = nout * 2 * ctw;  // P [o][d][2][L][N]
+  sign_combine_kernel<<<(unsigned)std::min<size_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(
+      w->d_P, w->d_A1, total, (int)p->logN, (int)L, limb_consts(p), sv, svsh);
+  HY_LAUNCH_CHECK();
+  PermDecompJob jd{w->d_P + ctw, w->d_D, w->d_C0, (int)L, (int)N, qarr(p), 2 * ctw};  // P_1 of every output
+  HY_TRY(launch_fwd(p, jd, nout * (L * L + L), s));
+  KsApplyArgs ka;
+  ka.c0 = w->d_C0;
+  ka.c0_stride = L * N;
+  ka.D = w->d_D;
+  ka.D_stride = L * L * N;
+  ka.diag = nullptr;
+  ka.diag_stride = 0;
+  ka.add = nullptr;
+  ka.add_stride = 0;
+  ka.key = w->d_swap_key;
+  ka.act = GaloisAct{0u, 1u};  // X -> X^{2N-1}: exchange the two slot rows
+  ka.out = w->d_X;
+  ka.L = (int)L;
+  ka.logN = (int)p->logN;
+  ka.total = nout * L * N;
+  ka.lcs = limb_consts(p);
+  HY_TRY(launch_ks_apply(ka, s));
+  OutInvAddJob jx{w->d_X, w->d_P, 2 * ctw, ct_out, (int)L, (int)N, qarr(p)};
+  return launch_inv(p, jx, nout * 2 * L, s);
 }
 
 hy_status finish_outputs(const hy_weights* w, size_t nunits, u64* ct_out, cudaStream_t s) {

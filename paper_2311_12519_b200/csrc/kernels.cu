@@ -412,6 +412,7 @@ struct KsMacArgs {
   const u64* sign;             // [L][N] sign plaintext (NTT), then [L][N] Shoup companions
   const int32_t* kt;           // fused tensor-core MAC: K term -> (tap << 16) | ct (-1 = padding)
   u64* out2;                   // coefficient-domain c_n = 2 (tc_coef): [A1] here, [A0] in out; else null
+  int coef;                    // 1x1 coefficient-domain MAC: C0 = the input cts [c][2][L][N] (R = ct)
   struct Taps {                // key pointers + automorphisms per tap, by value (no pointer chase)
     const u64* key[HY_MAX_TAPS];
     GaloisAct act[HY_MAX_TAPS];
@@ -1197,15 +1198,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mac_tc_kernel(KsMacArgs a, cons
   const int N = 1 << a.logN;
   const size_t LN = (size_t)a.L * N;
   const int tiles = N / TC_POS;
-  const int l = blockIdx.x / tiles, j0 = (blockIdx.x % tiles) * TC_POS;
-  const int mt = blockIdx.y, z = blockIdx.z;
+  // M tile fastest in the grid: the CTAs sharing an R column tile run together, so the tile is
+  // read from HBM once and from L2 by the other M tiles
+  const int nmt_ = (a.Mpad + 127) / 128;
+  const int mt = blockIdx.x % nmt_, ct_ = blockIdx.x / nmt_;
+  const int l = ct_ / tiles, j0 = (ct_ % tiles) * TC_POS;
+  const int z = blockIdx.z;
   const int nmt = (a.Mpad + 127) / 128;
   const int nchunks = a.Kpad / 32;
   const int tid = threadIdx.x, warp = tid >> 5;
 
   if (tid == 0) {
     for (int s = 0; s < TC_STAGES; s++) {
-      mbar_init(&full_bar[s], 128);
+      mbar_init(&full_bar[s], 4);  // one arrival per producer warp
       mbar_init(&empty_bar[s], 1);
     }
     mbar_init(&done_bar, 1);
@@ -1265,7 +1270,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mac_tc_kernel(KsMacArgs a, cons
 #pragma unroll
       for (int b = 0; b < 8; b++) *reinterpret_cast<uint2*>(&sB[s][b][boff]) = make_uint2(pa[b], pb[b]);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&full_bar[s]);
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&full_bar[s]);
     }
   } else if (tid == 128) {
     // ---------------- MMA issuer ----------------
@@ -1409,7 +1415,11 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
       pr[t].tap = tap;
       const u64* C0 = C0u + (size_t)c * LN;
       const u64* D = Du + (size_t)c * (LT * LN);
-      if (a.dbg & 4) {
+      if (a.coef) {  // 1x1 in the coefficient domain: R = the input ct itself (identity tap only)
+        const u64* ctp = a.C0 + ((size_t)z * a.Jcb + c) * 2 * LN + (size_t)l * N + j;
+        pr[t].c0 = __ldg(ctp);
+        pr[t].d[0] = __ldg(ctp + LN);
+      } else if (a.dbg & 4) {
         pr[t].c0 = c;
 #pragma unroll
         for (int i = 0; i < LT; i++) pr[t].d[i] = c + i;
@@ -1618,7 +1628,7 @@ hy_status launch_ksmac_tc(const KsMacArgs& a, const int8_t* w8, int units, cudaS
 
 hy_status launch_mac_tc(const KsMacArgs& a, const u64* R, const int8_t* w8, int units, cudaStream_t s) {
   const int N = 1 << a.logN;
-  dim3 grid((unsigned)(a.L * (N / TC_POS)), (unsigned)((a.Mpad + 127) / 128), (unsigned)units);
+  dim3 grid((unsigned)(a.L * (N / TC_POS) * ((a.Mpad + 127) / 128)), 1, (unsigned)units);
   mac_tc_kernel<<<grid, TC_THREADS, 0, s>>>(a, R, w8);
   HY_LAUNCH_CHECK();
   return HY_OK;
@@ -1890,9 +1900,24 @@ hy_status mac_coef(hy_weights* w, const u64* ct_in, size_t nunits, u64* ct_out, 
     a.out = w->d_P;
     a.out2 = w->d_A1;
   }
+  // the fused kernel's producers read the inputs directly (identity tap, no key switching): 12
+  // warps per CTA and 8 epilogue warps (the epilogue, one reduction per output coefficient,
+  // dominates a 1x1 layer)
+  a.coef = 1;
+  a.C0 = ct_in;
+  a.D = ct_in;
+  a.kt = w->d_kt;
+  a.tt.key[0] = nullptr;
+  a.tt.act[0] = GaloisAct{0u, 0u};
   HY_TRY(mac_mark(w, s));
   if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[0], s));
-  HY_TRY(launch_mac_tc(a, ct_in, w->d_w8, (int)nunits, s));
+  if (p->L == 2 || p->L == 3 || p->L == 5) {
+    HY_TRY(p->L == 2 ? launch_ksmac_tc<2>(a, w->d_w8, (int)nunits, s)
+           : p->L == 3 ? launch_ksmac_tc<3>(a, w->d_w8, (int)nunits, s)
+                       : launch_ksmac_tc<5>(a, w->d_w8, (int)nunits, s));
+  } else {
+    HY_TRY(launch_mac_tc(a, ct_in, w->d_w8, (int)nunits, s));
+  }
   if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[1], s));
   w->mac_launches = 1;
   return HY_OK;

@@ -1904,6 +1904,8 @@ hy_status mac_coef(hy_weights* w, const u64* ct_in, size_t nunits, u64* ct_out, 
   // warps per CTA and 8 epilogue warps (the epilogue, one reduction per output coefficient,
   // dominates a 1x1 layer)
   a.coef = 1;
+  static const int dbg = getenv("HY_DEBUG_KSMAC") ? atoi(getenv("HY_DEBUG_KSMAC")) : 0;
+  a.dbg = dbg;
   a.C0 = ct_in;
   a.D = ct_in;
   a.kt = w->d_kt;

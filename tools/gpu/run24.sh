@@ -10,5 +10,5 @@ for c in C1 C3a C3b C4 C5dw_4096 C5dw_8192 C5dw_16384 C5pw_4096 C5pw_8192 C5pw_1
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > gpurun_out/bench_reference.log 2>&1; echo "ref rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_C2.csv $B --config C2 --steps 3 > gpurun_out/ncu_launch_c2.log 2>&1; echo "ncu c2 rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_C4.csv $B --config C4 --steps 3 > gpurun_out/ncu_launch_c4.log 2>&1; echo "ncu c4 rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ksmac|PermDecomp|OutInv|StridedInv|DigitLift|ks_apply" -s 12 -c 6 -o gpurun_out/prof_C2_full $B --config C2 --steps 3 > gpurun_out/ncu_full_c2.log 2>&1; echo "ncu full c2 rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"ksmac_tc|PermDecomp|OutInv" -s 3 -c 3 -o gpurun_out/prof_C4_full $B --config C4 --steps 3 > gpurun_out/ncu_full_c4.log 2>&1; echo "ncu full c4 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"ksmac|PermDecomp|OutInv|StridedInv|DigitLift|ks_apply" -s 12 -c 6 -o gpurun_out/prof_C2_full $B --config C2 --steps 3 > gpurun_out/ncu_full_c2.log 2>&1; echo "ncu full c2 rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"ksmac_tc|PermDecomp|OutInv" -s 3 -c 3 -o gpurun_out/prof_C4_full $B --config C4 --steps 3 > gpurun_out/ncu_full_c4.log 2>&1; echo "ncu full c4 rc=$?"

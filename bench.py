@@ -273,7 +273,7 @@ MAC_KERNEL = {"thin": "ksmac_thin_kernel (fused S2+S3, FP64 MAC)",
               "tc_split": "mac_tc_kernel (S3 tcgen05 int8 MAC over stored R)",
               "fp64_fused": "ksmac_gemm_kernel (fused S2+S3, FP64 MAC)",
               "fp64_split": "mac_gemm_kernel (S3 FP64 MAC over stored R)",
-              "tc_coef": "mac_tc_kernel (1x1 c_n = 1: tcgen05 int8 MAC on the coefficient-form inputs, no NTT)"}
+              "tc_coef": "ksmac_tc_kernel (1x1: tcgen05 int8 MAC on the coefficient-form input cts, no key switching)"}
 
 
 def roofline(cfg, res, peaks, steps):

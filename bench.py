@@ -160,13 +160,14 @@ def run_gpu(args, cfg, rank, world):
         if args.mac_path:
             hy.hy_weights_set_mac_path(w, args.mac_path)
         mac_path = hy.hy_weights_mac_path(w)
-        hy.hy_weights_set_stage_events(w, ev)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     step_ms, stage_ms, mac_ms, mac_n = [], [[] for _ in range(3)], [], 0
     launches0 = hy.hy_kernel_launches()
+    # timed steps: no events inside the step (they would serialise the programmatic-dependent
+    # launches between the library's kernels)
     with ClockSampler(dev) as clk:
         for _ in range(args.steps):
             flush.zero_()                       # L2 flushed between timed iterations (untimed)
@@ -178,14 +179,24 @@ def run_gpu(args, cfg, rank, world):
             t1.record()
             t1.synchronize()
             step_ms.append(t0.elapsed_time(t1))
-            if w is not None:
-                for i in range(3):
-                    stage_ms[i].append(ev[i].elapsed_time(ev[i + 1]))
-                m, n = hy.hy_weights_mac_time(w)      # the MAC kernel's own launches
-                mac_ms.append(m)
-                mac_n += n
     torch.cuda.synchronize()
     launches = hy.hy_kernel_launches() - launches0
+    # per-stage / per-MAC-launch breakdown (rooflines): the same steps with the library's stage and
+    # MAC-launch events enabled, timed separately
+    if w is not None:
+        hy.hy_weights_set_stage_events(w, ev)
+        for it in range(min(args.steps, 10) + 1):
+            flush.zero_()
+            torch.cuda.synchronize()
+            step()
+            torch.cuda.synchronize()
+            if it == 0:
+                continue                        # first run with events: warm-up
+            for i in range(3):
+                stage_ms[i].append(ev[i].elapsed_time(ev[i + 1]))
+            m, n = hy.hy_weights_mac_time(w)      # the MAC kernel's own launches
+            mac_ms.append(m)
+            mac_n += n
     total_ms = sum(step_ms)
     if dist is not None:
         t = torch.tensor([total_ms, float(launches)], dtype=torch.float64, device=device)
@@ -292,7 +303,7 @@ def roofline(cfg, res, peaks, steps):
     clk_mhz = res["clocks"].get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
     int_peak = MODMUL_PER_CLK_SM * SM_COUNT * clk_mhz * 1e6 / 1e9          # Gmodmul/s
     mac_ms = res["mac_ms"] or st["S2S3_ksmac_wht"]
-    per_step = max(1, res["mac_launches"] // max(1, steps))
+    per_step = max(1, res["mac_launches"] // max(1, min(steps, 10)))
     dom = max(st, key=st.get)
     kernels = {}
     if path == "tc_coef":           # 1x1 coefficient-domain MAC: no S1; c_n = 2 keeps the row swap

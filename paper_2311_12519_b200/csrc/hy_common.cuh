@@ -174,6 +174,42 @@ struct hy_weights {
 };
 
 // ------------------------------------------------------------------------------------
+// programmatic dependent launch: every kernel of the hy_conv_eval chain lets its successor
+// launch as soon as all its CTAs are resident, and waits for its predecessor's completion (and
+// memory) before touching the predecessor's outputs.  Both are no-ops for a normal launch.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// launch with cudaLaunchAttributeProgrammaticStreamSerialization (optionally in clusters of cx)
+template <typename... KArgs, typename... Args>
+inline cudaError_t hy_launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cx,
+                             Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[n].val.programmaticStreamSerializationAllowed = 1;
+  n++;
+  if (cx > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = cx;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    n++;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+// ------------------------------------------------------------------------------------
 // device modular arithmetic
 // ------------------------------------------------------------------------------------
 __device__ __forceinline__ u64 shoup_mul(u64 x, u64 w, u64 w_sh, u64 q) {

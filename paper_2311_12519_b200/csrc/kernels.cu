@@ -155,6 +155,7 @@ struct KsApplyArgs {
 
 template <int LT>
 __global__ void __launch_bounds__(256) ks_apply_kernel(KsApplyArgs a) {
+  pdl_begin();
   const size_t idx = (size_t)blockIdx.x * 256 + threadIdx.x;
   if (idx >= a.total) return;
   const int N = 1 << a.logN, L = LT > 0 ? LT : a.L;
@@ -193,10 +194,10 @@ hy_status launch_ks_apply(const KsApplyArgs& a, cudaStream_t s) {
   if (!a.total) return HY_OK;
   const unsigned blocks = (unsigned)((a.total + 255) / 256);
   switch (a.L) {  // compile-time digit count: all loads of a thread issue at once
-    case 2: ks_apply_kernel<2><<<blocks, 256, 0, s>>>(a); break;
-    case 3: ks_apply_kernel<3><<<blocks, 256, 0, s>>>(a); break;
-    case 5: ks_apply_kernel<5><<<blocks, 256, 0, s>>>(a); break;
-    default: ks_apply_kernel<0><<<blocks, 256, 0, s>>>(a); break;
+    case 2: HY_CUDA_TRY(hy_launch(ks_apply_kernel<2>, dim3(blocks), dim3(256), 0, s, 1, a)); break;
+    case 3: HY_CUDA_TRY(hy_launch(ks_apply_kernel<3>, dim3(blocks), dim3(256), 0, s, 1, a)); break;
+    case 5: HY_CUDA_TRY(hy_launch(ks_apply_kernel<5>, dim3(blocks), dim3(256), 0, s, 1, a)); break;
+    default: HY_CUDA_TRY(hy_launch(ks_apply_kernel<0>, dim3(blocks), dim3(256), 0, s, 1, a)); break;
   }
   HY_LAUNCH_CHECK();
   return HY_OK;
@@ -318,7 +319,8 @@ hy_status launch_fwd_t(const hy_params* p, const Job& job, size_t npoly, cudaStr
     HY_CUDA_TRY(cudaFuncSetAttribute(ntt_fwd_kernel<LOGN, Job>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attr_done = true;
   }
-  ntt_fwd_kernel<LOGN, Job><<<(unsigned)(npoly * C::S), C::T, sm, s>>>(job, p->tab, limb_consts(p));
+  HY_CUDA_TRY(hy_launch(ntt_fwd_kernel<LOGN, Job>, dim3((unsigned)(npoly * C::S)), dim3(C::T), sm, s, 1, job, p->tab,
+                        limb_consts(p)));
   HY_LAUNCH_CHECK();
   return HY_OK;
 }
@@ -333,19 +335,8 @@ hy_status launch_inv_t(const hy_params* p, const Job& job, size_t npoly, cudaStr
     HY_CUDA_TRY(cudaFuncSetAttribute(ntt_inv_kernel<LOGN, Job>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     attr_done = true;
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(npoly * C::S));
-  cfg.blockDim = dim3(C::T);
-  cfg.dynamicSmemBytes = sm;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = C::S;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  HY_CUDA_TRY(cudaLaunchKernelEx(&cfg, ntt_inv_kernel<LOGN, Job>, job, p->tab, limb_consts(p)));
+  HY_CUDA_TRY(hy_launch(ntt_inv_kernel<LOGN, Job>, dim3((unsigned)(npoly * C::S)), dim3(C::T), sm, s, C::S, job,
+                        p->tab, limb_consts(p)));
   HY_LAUNCH_CHECK();
   return HY_OK;
 }
@@ -597,6 +588,7 @@ __device__ __forceinline__ void store_outputs(const KsMacArgs& a, int z, int row
 // key switching (INT pipes, L2 loads) overlaps the other's DFMAs.
 template <int WM, int LT>
 __global__ void __launch_bounds__(256, 2) ksmac_gemm_kernel(KsMacArgs a) {
+  pdl_begin();
   constexpr int BM = 8 * WM, PG = 8 / WM, BNP = 32 * PG, KC = 2 * WM;
   static_assert(KC * BNP == 512, "two R items per thread per chunk");
   constexpr int NL = LT > 0 ? LT : 1;
@@ -798,6 +790,7 @@ __global__ void __launch_bounds__(256, 2) ksmac_gemm_kernel(KsMacArgs a) {
 // key switching of the first.
 template <int MR, int LT, int CPT>
 __global__ void __launch_bounds__(256) ksmac_thin_kernel(KsMacArgs a, int units) {
+  pdl_begin();
   const int N = 1 << a.logN;
   const int idx = blockIdx.x * 256 + threadIdx.x;
   const int l = idx >> a.logN, j = idx & (N - 1);
@@ -1354,6 +1347,7 @@ inline size_t kt_smem(int T, int L) { return KT_SMEM_MMA + (size_t)T * 4 * L * T
 
 template <int LT, int LOGN>  // LOGN > 0: compile-time ring degree (address math folds into immediates)
 __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, const int8_t* __restrict__ w8) {
+  pdl_begin();
   extern __shared__ uint8_t kt_dyn[];
   uint8_t* smb = reinterpret_cast<uint8_t*>(((uintptr_t)kt_dyn + 1023) & ~(uintptr_t)1023);
   auto sA = [&](int s, int ks) { return smb + (size_t)s * (KT_STAGE_A + KT_STAGE_B) + ks * 4096; };
@@ -1614,7 +1608,7 @@ hy_status launch_ksmac_tc_t(const KsMacArgs& a, const int8_t* w8, int units, cud
     attr_done = true;
   }
   dim3 grid((unsigned)(a.L * (N / TC_POS)), (unsigned)((a.Mpad + 127) / 128), (unsigned)units);
-  ksmac_tc_kernel<LT, LOGN><<<grid, KT_THREADS, kt_smem(a.T, LT), s>>>(a, w8);
+  HY_CUDA_TRY(hy_launch(ksmac_tc_kernel<LT, LOGN>, grid, dim3(KT_THREADS), kt_smem(a.T, LT), s, 1, a, w8));
   HY_LAUNCH_CHECK();
   return HY_OK;
 }
@@ -1669,7 +1663,7 @@ hy_status launch_ksmac_gemm_t(const KsMacArgs& a, int units, cudaStream_t s) {
     attr = sm;
   }
   dim3 grid((unsigned)(a.L * (N / BNP)), (unsigned)(a.Mpad / (8 * WM)), (unsigned)units);
-  ksmac_gemm_kernel<WM, LT><<<grid, 256, sm, s>>>(a);
+  HY_CUDA_TRY(hy_launch(ksmac_gemm_kernel<WM, LT>, grid, dim3(256), sm, s, 1, a));
   HY_LAUNCH_CHECK();
   return HY_OK;
 }
@@ -1688,7 +1682,7 @@ hy_status launch_ksmac_thin(const KsMacArgs& a, int units, cudaStream_t s) {
   const int N = 1 << a.logN;
   constexpr int CPT = LT == 5 ? 2 : 4;  // units per thread (registers: CPT x (L + 1) digits + 4 MR sums)
   dim3 grid((unsigned)((a.L * N + 255) / 256), 1, (unsigned)((units + CPT - 1) / CPT));
-  ksmac_thin_kernel<MR, LT, CPT><<<grid, 256, 0, s>>>(a, units);
+  HY_CUDA_TRY(hy_launch(ksmac_thin_kernel<MR, LT, CPT>, grid, dim3(256), 0, s, 1, a, units));
   HY_LAUNCH_CHECK();
   return HY_OK;
 }
@@ -1858,6 +1852,7 @@ hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
 // negacyclic sign for wrapped indices.  In place over P (= A0) [n][2][L][N]; canonical output.
 __global__ void sign_combine_kernel(u64* __restrict__ P, const u64* __restrict__ A1, size_t total, int logN, int L,
                                     LimbConsts lcs, QArr sv, QArr svsh) {
+  pdl_begin();
   const int N = 1 << logN;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
     const int j = (int)(i & (N - 1));
@@ -1940,8 +1935,9 @@ hy_status finish_coef2(const hy_weights* w, size_t nunits, u64* ct_out, cudaStre
     svsh.q[l] = (u64)(((u128)sv.q[l] << 64) / q);
   }
   const size_t total = nout * 2 * ctw;  // P [o][d][2][L][N]
-  sign_combine_kernel<<<(unsigned)std::min<size_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(
-      w->d_P, w->d_A1, total, (int)p->logN, (int)L, limb_consts(p), sv, svsh);
+  HY_CUDA_TRY(hy_launch(sign_combine_kernel, dim3((unsigned)std::min<size_t>((total + 255) / 256, 148 * 16)),
+                        dim3(256), 0, s, 1, w->d_P, (const u64*)w->d_A1, total, (int)p->logN, (int)L,
+                        limb_consts(p), sv, svsh));
   HY_LAUNCH_CHECK();
   PermDecompJob jd{w->d_P + ctw, w->d_D, w->d_C0, (int)L, (int)N, qarr(p), 2 * ctw};  // P_1 of every output
   HY_TRY(launch_fwd(p, jd, nout * (L * L + L), s));

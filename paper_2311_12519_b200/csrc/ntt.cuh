@@ -81,6 +81,7 @@ struct NttCfg {
 // ---------------------------------------------------------------------------------------
 template <int LOGN, class Job>
 __global__ void __launch_bounds__(NttCfg<LOGN>::T) ntt_fwd_kernel(Job job, DevTables tab, LimbConsts L) {
+  pdl_begin();
   using C = NttCfg<LOGN>;
   constexpr int S = C::S, B = C::B, V = C::V, T = C::T;
   extern __shared__ u64 sm[];
@@ -187,6 +188,7 @@ __global__ void __launch_bounds__(NttCfg<LOGN>::T) ntt_fwd_kernel(Job job, DevTa
 // ---------------------------------------------------------------------------------------
 template <int LOGN, class Job>
 __global__ void __launch_bounds__(NttCfg<LOGN>::T) ntt_inv_kernel(Job job, DevTables tab, LimbConsts L) {
+  pdl_begin();
   using C = NttCfg<LOGN>;
   constexpr int S = C::S, B = C::B, V = C::V, T = C::T;
   extern __shared__ u64 sm[];

@@ -178,9 +178,11 @@ struct hy_weights {
 // launch as soon as all its CTAs are resident, and waits for its predecessor's completion (and
 // memory) before touching the predecessor's outputs.  Both are no-ops for a normal launch.
 // ------------------------------------------------------------------------------------
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_begin() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  pdl_trigger();
+  pdl_wait();
 }
 
 // launch with cudaLaunchAttributeProgrammaticStreamSerialization (optionally in clusters of cx)

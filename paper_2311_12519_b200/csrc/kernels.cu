@@ -588,7 +588,7 @@ __device__ __forceinline__ void store_outputs(const KsMacArgs& a, int z, int row
 // key switching (INT pipes, L2 loads) overlaps the other's DFMAs.
 template <int WM, int LT>
 __global__ void __launch_bounds__(256, 2) ksmac_gemm_kernel(KsMacArgs a) {
-  pdl_begin();
+  pdl_trigger();  // the key staging below reads only uploaded keys: it overlaps the predecessor
   constexpr int BM = 8 * WM, PG = 8 / WM, BNP = 32 * PG, KC = 2 * WM;
   static_assert(KC * BNP == 512, "two R items per thread per chunk");
   constexpr int NL = LT > 0 ? LT : 1;
@@ -621,6 +621,7 @@ __global__ void __launch_bounds__(256, 2) ksmac_gemm_kernel(KsMacArgs a) {
     }
   }
   __syncthreads();
+  pdl_wait();  // D, C0 come from PermDecomp
 
   // Every thread produces the items (kkl, p) = (tid / BNP + 256 h / BNP, tid % BNP), h = 0, 1:
   // always the same position p.  LT > 0: the digit reads of chunk ch + 1 are issued before the
@@ -1347,7 +1348,7 @@ inline size_t kt_smem(int T, int L) { return KT_SMEM_MMA + (size_t)T * 4 * L * T
 
 template <int LT, int LOGN>  // LOGN > 0: compile-time ring degree (address math folds into immediates)
 __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, const int8_t* __restrict__ w8) {
-  pdl_begin();
+  pdl_trigger();  // key staging and TMEM setup read only uploaded data: they overlap the predecessor
   extern __shared__ uint8_t kt_dyn[];
   uint8_t* smb = reinterpret_cast<uint8_t*>(((uintptr_t)kt_dyn + 1023) & ~(uintptr_t)1023);
   auto sA = [&](int s, int ks) { return smb + (size_t)s * (KT_STAGE_A + KT_STAGE_B) + ks * 4096; };
@@ -1433,8 +1434,6 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
       tap0++;
     }
   };
-  // the first chunk's digit reads are in flight while the keys are staged and TMEM is set up
-  load_chunk(0, pre);
 
   for (int t = tid; t < a.T; t += KT_THREADS) {
     s_haskey[t] = a.tt.key[t] != nullptr;
@@ -1474,6 +1473,8 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  pdl_wait();  // D, C0 (or the input cts) come from the predecessor
+  load_chunk(0, pre);
 
   const uint32_t idesc = umma_idesc_s8u8(128, 8 * TC_COLS);  // one UMMA covers the 8 byte planes
   // one register buffer (occupancy first: 2 CTAs x 12 warps per SM): the next chunk's digit

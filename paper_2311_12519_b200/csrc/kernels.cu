@@ -416,13 +416,11 @@ struct KsMacArgs {
 constexpr uint32_t M30 = 0x3FFFFFFFu;
 
 __device__ __forceinline__ u64 reduce_wide(long long H, long long Lo, const LimbConst& c) {
-  // value H * 2^30 + Lo (|H|, |Lo| < 2^59) mod q, canonical
-  const u64 hu = (u64)(H + (long long)c.off);
-  const u64 lu = (u64)(Lo + (long long)c.off);
-  u64 a = shoup_mul(hu, c.c30, c.c30_sh, c.q);  // [0, 2q)
-  u64 b = reduce_2q(lu, c.one_sh, c.q);         // [0, 2q)
-  u64 s = csub(a + b, c.two_q);
-  return csub(s, c.q);
+  // value H * 2^30 + Lo (|H|, |Lo| < 2^59) mod q, canonical: Lo's bits above 30 are folded into H
+  // (|H + Lo / 2^30| < 2^60 < off62), so ONE Shoup product by 2^30 mod q reduces the value
+  const long long h2 = H + (Lo >> 30);
+  const u64 a = shoup_mul((u64)(h2 + (long long)c.off62), c.c30, c.c30_sh, c.q);  // [0, 2q)
+  return csub(csub(a + (u64)(Lo & 0x3fffffffll), c.two_q), c.q);                 // < 2q + 2^30
 }
 
 // Key words of tap t for limb l at slot position j: digit i, component comp at
@@ -1144,11 +1142,12 @@ __device__ __forceinline__ void tc_store(const KsMacArgs& a, int z, int row, int
   const int N = LOGN > 0 ? (1 << LOGN) : (1 << a.logN);
   const size_t LN = (size_t)(LT > 0 ? LT : a.L) * N;
   const LimbConst& c = a.lcs.lc[l];
-  auto red = [&](long long h, long long lo) -> u64 {  // |h|, |lo| < 2^62
-    const u64 hu = (u64)(h + (long long)c.off62), lu = (u64)(lo + (long long)c.off62);
-    const u64 x = shoup_mul(hu, c.c32, c.c32_sh, c.q);
-    const u64 y = reduce_2q(lu, c.one_sh, c.q);
-    return csub(csub(x + y, c.two_q), c.q);
+  auto red = [&](long long h, long long lo) -> u64 {  // h 2^32 + lo mod q, |h| < 2^61, |lo| < 2^62
+    // fold lo's high word into h: value = (h + lo_hi) 2^32 + lo_lo with lo_lo in [0, 2^32), so ONE
+    // Shoup product by 2^32 mod q reduces it (|h + lo_hi| < 2^62 = off62 bound, off62 = 0 mod q)
+    const long long h2 = h + (lo >> 32);
+    const u64 x = shoup_mul((u64)(h2 + (long long)c.off62), c.c32, c.c32_sh, c.q);  // [0, 2q)
+    return csub(csub(x + (u64)(lo & 0xffffffffll), c.two_q), c.q);  // < 2q + 2^32 < 3q
   };
   if (a.cn == 1) {
     if (row < a.M) a.out[((size_t)(z * a.M + row) * 2 + comp) * LN + (size_t)l * N + j] = red(H, Lo);

@@ -1340,7 +1340,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) mac_tc_kernel(KsMacArgs a, cons
 // its 2 x 8 UMMAs (M = 128, N = 32, K = 32, s8 x u8 -> s32) into the 8 TMEM accumulators.  TMEM is
 // zeroed first and every UMMA accumulates: integer sums are exact, so the issue order of chunks by
 // different warps does not matter.
-constexpr int KT_THREADS = 256, KT_WARPS = KT_THREADS / 32, KT_STAGES = 3, KT_KS = 2, KT_CHUNK = 32 * KT_KS;
+constexpr int KT_THREADS = 384, KT_WARPS = KT_THREADS / 32, KT_STAGES = 2, KT_KS = 3, KT_CHUNK = 32 * KT_KS;
 constexpr int KT_STAGE_A = KT_KS * 4096, KT_STAGE_B = KT_KS * 8 * 1024;
 constexpr size_t KT_SMEM_MMA = (size_t)KT_STAGES * (KT_STAGE_A + KT_STAGE_B) + 1024;
 inline size_t kt_smem(int T, int L) { return KT_SMEM_MMA + (size_t)T * 4 * L * TC_POS * sizeof(u64); }
@@ -1459,13 +1459,17 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = s_tmem;
-  const int quad = warp & 3, chalf = warp >> 2;  // TMEM lanes 32 quad .. and columns half chalf
+  // TMEM work split: warp w owns lane quadrant w % 4 (the tcgen05.ld/st lane restriction) and
+  // every KT_WARPS / 4-th group of columns of it, so all 12 warps share the zeroing and the epilogue
+  constexpr int KT_PARTS = KT_WARPS / 4;
+  static_assert(KT_WARPS % 4 == 0, "whole lane quadrants");
+  const int quad = warp & 3, part = warp >> 2;
   const bool rows_live = mt * 128 + quad * 32 < a.M;  // rows >= M are padding: never read back
-  if (warp < 8 && rows_live) {
-    const uint32_t zb = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(chalf * TC_TMEM_COLS / 2);
+  if (rows_live) {
+    const uint32_t zb = tmem + ((uint32_t)(quad * 32) << 16);
     const uint32_t z0 = 0;
 #pragma unroll 1
-    for (int c = 0; c < (int)TC_TMEM_COLS / 2; c += 8)
+    for (int c = part * 8; c < (int)TC_TMEM_COLS; c += 8 * KT_PARTS)
       asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(zb + c), "r"(z0)
                    : "memory");
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -1567,12 +1571,11 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   for (int ch = nchunks > KT_STAGES ? nchunks - KT_STAGES : 0; ch < nchunks; ch++)
     mbar_wait(&empty_bar[ch % KT_STAGES], (ch / KT_STAGES) & 1);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (warp < 8 && rows_live && !(a.dbg & 8)) {
-    const int comp = chalf;
+  if (rows_live && !(a.dbg & 8)) {
     const int row = mt * 128 + quad * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
-    for (int c0 = comp * 16; c0 < comp * 16 + 16; c0 += 4) {
+    for (int c0 = part * 4; c0 < TC_COLS; c0 += 4 * KT_PARTS) {  // groups of 4 columns
       uint32_t v[8][4];  // [plane][column]
 #pragma unroll
       for (int b = 0; b < 8; b++) {

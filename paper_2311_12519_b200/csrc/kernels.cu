@@ -1171,6 +1171,61 @@ __device__ __forceinline__ void tc_store(const KsMacArgs& a, int z, int row, int
   a.out[((size_t)(z * (a.M / 2) + row / 2) * 2 + comp) * LN + (size_t)l * N + j] = v;
 }
 
+// tc_store for 4 consecutive positions j .. j + 3 (j % 4 == 0) of one component: the same
+// arithmetic, written as two 16-byte stores per row instead of four 8-byte ones
+template <int LT = 0, int LOGN = 0>
+__device__ __forceinline__ void tc_store4(const KsMacArgs& a, int z, int row, int comp, int l, int j,
+                                          const long long* H, const long long* Lo) {
+  const int N = LOGN > 0 ? (1 << LOGN) : (1 << a.logN);
+  const size_t LN = (size_t)(LT > 0 ? LT : a.L) * N;
+  const LimbConst& c = a.lcs.lc[l];
+  auto red = [&](long long h, long long lo) -> u64 {  // as in tc_store: one Shoup product
+    const long long h2 = h + (lo >> 32);
+    const u64 x = shoup_mul((u64)(h2 + (long long)c.off62), c.c32, c.c32_sh, c.q);
+    return csub(csub(x + (u64)(lo & 0xffffffffll), c.two_q), c.q);
+  };
+  u64 v[4];
+  if (a.cn == 1) {
+    if (row >= a.M) return;
+#pragma unroll
+    for (int i = 0; i < 4; i++) v[i] = red(H[i], Lo[i]);
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(a.out + ((size_t)(z * a.M + row) * 2 + comp) * LN + (size_t)l * N + j);
+    dst[0] = make_ulonglong2(v[0], v[1]);
+    dst[1] = make_ulonglong2(v[2], v[3]);
+    return;
+  }
+  long long H1[4], L1[4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    H1[i] = __shfl_xor_sync(0xffffffffu, H[i], 1);
+    L1[i] = __shfl_xor_sync(0xffffffffu, Lo[i], 1);
+  }
+  if ((row & 1) || row >= a.M) return;
+  const long long k = a.kscale;
+  u64 a0[4], a1[4];
+#pragma unroll
+  for (int i = 0; i < 4; i++) {  // Walsh-Hadamard on the exact accumulators (Eq. 2)
+    a0[i] = red(k * (H[i] + H1[i]), k * (Lo[i] + L1[i]));
+    a1[i] = red(H[i] - H1[i], Lo[i] - L1[i]);
+  }
+  const size_t at = ((size_t)(z * (a.M / 2) + row / 2) * 2 + comp) * LN + (size_t)l * N + j;
+  if (a.out2) {  // coefficient domain: the sign PMult is applied by sign_combine
+    reinterpret_cast<ulonglong2*>(a.out + at)[0] = make_ulonglong2(a0[0], a0[1]);
+    reinterpret_cast<ulonglong2*>(a.out + at)[1] = make_ulonglong2(a0[2], a0[3]);
+    reinterpret_cast<ulonglong2*>(a.out2 + at)[0] = make_ulonglong2(a1[0], a1[1]);
+    reinterpret_cast<ulonglong2*>(a.out2 + at)[1] = make_ulonglong2(a1[2], a1[3]);
+    return;
+  }
+  const ulonglong2* sp = reinterpret_cast<const ulonglong2*>(a.sign + (size_t)l * N + j);
+  const ulonglong2* ssp = reinterpret_cast<const ulonglong2*>(a.sign + LN + (size_t)l * N + j);
+  const ulonglong2 s01 = __ldg(sp), s23 = __ldg(sp + 1), h01 = __ldg(ssp), h23 = __ldg(ssp + 1);
+  const u64 sg[4] = {s01.x, s01.y, s23.x, s23.y}, sgs[4] = {h01.x, h01.y, h23.x, h23.y};
+#pragma unroll
+  for (int i = 0; i < 4; i++) v[i] = csub(csub(a0[i] + shoup_mul(a1[i], sg[i], sgs[i], c.q), c.two_q), c.q);
+  reinterpret_cast<ulonglong2*>(a.out + at)[0] = make_ulonglong2(v[0], v[1]);
+  reinterpret_cast<ulonglong2*>(a.out + at)[1] = make_ulonglong2(v[2], v[3]);
+}
+
 // 4x4 byte transpose: w[b] = byte b of x[0], x[1], x[2], x[3]
 __device__ __forceinline__ void byte_tr4(const uint32_t* x, uint32_t* w) {
   const uint32_t t0 = __byte_perm(x[0], x[1], 0x5140), t1 = __byte_perm(x[0], x[1], 0x7362);
@@ -1584,6 +1639,7 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
                      : "r"(lane_base + (uint32_t)(b * TC_COLS + c0)));
       }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      long long lo4[4], hi4[4];
 #pragma unroll
       for (int cc = 0; cc < 4; cc++) {
         long long lo = 0, hi = 0;
@@ -1591,9 +1647,10 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
         for (int b = 0; b < 4; b++) lo += (long long)(int32_t)v[b][cc] << (8 * b);
 #pragma unroll
         for (int b = 4; b < 8; b++) hi += (long long)(int32_t)v[b][cc] << (8 * (b - 4));
-        const int col = c0 + cc;
-        tc_store<LT, LOGN>(a, z, row, col >> 4, l, j0 + (col & 15), hi, lo);
+        lo4[cc] = lo;
+        hi4[cc] = hi;
       }
+      tc_store4<LT, LOGN>(a, z, row, c0 >> 4, l, j0 + (c0 & 15), hi4, lo4);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1911,10 +1968,8 @@ hy_status mac_coef(hy_weights* w, const u64* ct_in, size_t nunits, u64* ct_out, 
   a.tt.act[0] = GaloisAct{0u, 0u};
   HY_TRY(mac_mark(w, s));
   if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[0], s));
-  if (p->L == 2 || p->L == 3 || p->L == 5) {
-    HY_TRY(p->L == 2 ? launch_ksmac_tc<2>(a, w->d_w8, (int)nunits, s)
-           : p->L == 3 ? launch_ksmac_tc<3>(a, w->d_w8, (int)nunits, s)
-                       : launch_ksmac_tc<5>(a, w->d_w8, (int)nunits, s));
+  if (p->L == 2 || p->L == 3) {  // (L = 5 spills at 12 warps x 80 registers: the older MAC kernel)
+    HY_TRY(p->L == 2 ? launch_ksmac_tc<2>(a, w->d_w8, (int)nunits, s) : launch_ksmac_tc<3>(a, w->d_w8, (int)nunits, s));
   } else {
     HY_TRY(launch_mac_tc(a, ct_in, w->d_w8, (int)nunits, s));
   }

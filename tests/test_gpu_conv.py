@@ -193,3 +193,81 @@ def test_empty_and_misaligned_inputs(hy):
             hy.hy_weights_destroy(w)
     finally:
         hy.hy_params_destroy(p)
+
+
+def test_streams_and_shared_params(hy):
+    """ABI conventions (include/hyena.h): params and keys are shared by several weight handles; two
+    layers evaluated concurrently on two non-default streams (stream-ordered, no host sync) give
+    the oracle's bits; re-evaluating with the same handles is deterministic."""
+    c1 = dict(CASES["cn2_blocks"])
+    N, bits, L = c1.pop("N"), c1.pop("bits"), c1.pop("L")
+    primes = ntt_primes(N, bits, L)
+    lay1 = make_layer(N, primes, seed=580, **c1)
+    c2 = dict(c1, Co=6)
+    lay2 = make_layer(N, primes, seed=580, **c2)  # same seed: same secret and keys, other weights
+    assert sorted(lay1.keys) == sorted(lay2.keys)
+    p = hy.hy_params_create(N, primes, 65537)
+    try:
+        elts = list(lay1.keys)
+        hy.hy_keys_upload(p, elts, np.stack([lay1.keys[g] for g in elts]))
+        w1 = hy.hy_encode_weights(p, lay1.W, **shape_of(lay1))
+        w2 = hy.hy_encode_weights(p, lay2.W, **shape_of(lay2))
+        try:
+            outs = {}
+            s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+            for name, w, lay, st in (("a", w1, lay1, s1), ("b", w2, lay2, s2)):
+                Lw = hy.hy_weights_layout(w)
+                ct_in = torch.from_numpy(lay.ct_in).cuda()
+                ct_out = torch.zeros((Lw.Jout, 2, L, N), dtype=torch.uint64, device="cuda")
+                torch.cuda.synchronize()
+                with torch.cuda.stream(st):
+                    hy.hy_conv_eval(w, ct_in, ct_out, stream=st.cuda_stream)
+                outs[name] = (ct_in, ct_out, lay, Lw)
+            torch.cuda.synchronize()
+            for name, (ct_in, ct_out, lay, Lw) in outs.items():
+                ref = conv.he_conv(lay.P, lay.ls, lay.W, lay.ct_in, lay.keys)
+                got = ct_out.cpu().numpy()
+                for i in range(Lw.Jout):
+                    assert np.array_equal(got[i], ref[i]), f"layer {name} ct {i}"
+            # second evaluation of layer a (buffers reused): bit-identical
+            ct_in, ct_out, lay, Lw = outs["a"]
+            again = torch.zeros_like(ct_out)
+            hy.hy_conv_eval(w1, ct_in, again)
+            torch.cuda.synchronize()
+            assert torch.equal(again, ct_out)
+        finally:
+            hy.hy_weights_destroy(w1)
+            hy.hy_weights_destroy(w2)
+    finally:
+        hy.hy_params_destroy(p)
+
+
+def test_key_reupload_rebinds(hy):
+    """Uploading new switching keys after hy_encode_weights is picked up by the next evaluation
+    (the weights' tap-key table is rebound), and the result matches the oracle with the new keys."""
+    c = dict(CASES["cn1_blocks_tail"])
+    N, bits, L = c.pop("N"), c.pop("bits"), c.pop("L")
+    primes = ntt_primes(N, bits, L)
+    lay = make_layer(N, primes, seed=590, **c)
+    p = hy.hy_params_create(N, primes, 65537)
+    try:
+        elts = list(lay.keys)
+        junk = {g: synth.gen_uniform_keys(primes, 1, N, 99, stream=n)[0] for n, g in enumerate(elts)}
+        hy.hy_keys_upload(p, elts, np.stack([junk[g] for g in elts]))
+        w = hy.hy_encode_weights(p, lay.W, **shape_of(lay))
+        try:
+            Lw = hy.hy_weights_layout(w)
+            ct_in = torch.from_numpy(lay.ct_in).cuda()
+            ct_out = torch.zeros((Lw.Jout, 2, L, N), dtype=torch.uint64, device="cuda")
+            hy.hy_conv_eval(w, ct_in, ct_out)              # with the junk keys
+            hy.hy_keys_upload(p, elts, np.stack([lay.keys[g] for g in elts]))
+            hy.hy_conv_eval(w, ct_in, ct_out)              # must use the real keys now
+            torch.cuda.synchronize()
+            ref = conv.he_conv(lay.P, lay.ls, lay.W, lay.ct_in, lay.keys)
+            got = ct_out.cpu().numpy()
+            for i in range(Lw.Jout):
+                assert np.array_equal(got[i], ref[i])
+        finally:
+            hy.hy_weights_destroy(w)
+    finally:
+        hy.hy_params_destroy(p)

@@ -1450,8 +1450,50 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
     int tap;  // -1 = padding term (R = 0); identity tap: d[0] = D_{c,l}
   };
   Term pre[4];
+  int grp = -1;  // >= 0: this chunk's 4 terms are consecutive cts of tap grp, all < K (fast path)
   auto load_chunk = [&](int ch, Term* pr) {
     int tap = tap0, c = c0t;
+    // common case: the thread's 4 terms share one tap (no ct wrap) and are all real terms: one
+    // permutation and base address, strided loads, no per-term tests
+    grp = (c0t + 3 < a.Jcb && ch * KT_CHUNK + tg * 4 + 3 < a.K && !a.dbg) ? tap0 : -1;
+    if (grp >= 0 && a.coef) {  // 1x1 coefficient domain: R = the 4 input cts themselves
+      const u64* ctp = a.C0 + ((size_t)z * a.Jcb + c) * 2 * LN + (size_t)l * N + j;
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        pr[t].tap = tap;
+        pr[t].c0 = __ldg(ctp + (size_t)t * 2 * LN);
+        pr[t].d[0] = __ldg(ctp + (size_t)t * 2 * LN + LN);
+      }
+      c0t += KT_CHUNK;
+      while (c0t >= a.Jcb) {
+        c0t -= a.Jcb;
+        tap0++;
+      }
+      return;
+    }
+    if (grp >= 0) {
+      const u64* C0 = C0u + (size_t)c * LN;
+      const u64* D = Du + (size_t)c * (LT * LN);
+      const bool ident = a.tt.key[tap] == nullptr;
+      const int jp = ident ? j : galois_perm(j, a.tt.act[tap], N >> 1);
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        pr[t].tap = tap;
+        pr[t].c0 = __ldg(C0 + (size_t)t * LN + jp);
+        if (ident) {
+          pr[t].d[0] = __ldg(D + (size_t)t * LT * LN + l * LN + j);
+        } else {
+#pragma unroll
+          for (int i = 0; i < LT; i++) pr[t].d[i] = __ldg(D + (size_t)t * LT * LN + i * LN + jp);
+        }
+      }
+      c0t += KT_CHUNK;
+      while (c0t >= a.Jcb) {
+        c0t -= a.Jcb;
+        tap0++;
+      }
+      return;
+    }
 #pragma unroll
     for (int t = 0; t < 4; t++) {
       if (t > 0 && ++c >= a.Jcb) {
@@ -1556,6 +1598,22 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
     // R (byte planes), and the epilogue's single reduction makes the output canonical, so R
     // needs no reduction at all.
     uint32_t lo0[4], hi0[4], lo1[4], hi1[4];
+    if (grp >= 0 && s_haskey[grp]) {  // fast path: one tap, 4 real terms, keys at one address
+      const u64* kp = skey + (size_t)grp * 4 * LT * TC_POS + pos;
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        u64 r0 = cur[t].c0, r1 = 0;
+#pragma unroll
+        for (int i = 0; i < LT; i++) {
+          r0 += shoup_mul(cur[t].d[i], kp[(4 * i) * TC_POS], kp[(4 * i + 1) * TC_POS], q);
+          r1 += shoup_mul(cur[t].d[i], kp[(4 * i + 2) * TC_POS], kp[(4 * i + 3) * TC_POS], q);
+        }
+        lo0[t] = (uint32_t)r0;
+        hi0[t] = (uint32_t)(r0 >> 32);
+        lo1[t] = (uint32_t)r1;
+        hi1[t] = (uint32_t)(r1 >> 32);
+      }
+    } else
 #pragma unroll
     for (int t = 0; t < 4; t++) {
       const int tap = cur[t].tap;

@@ -222,6 +222,16 @@ __device__ __forceinline__ u64 shoup_mul(u64 x, u64 w, u64 w_sh, u64 q) {
 
 __device__ __forceinline__ u64 csub(u64 x, u64 m) { return x >= m ? x - m : x; }
 
+// canonical residue of a lazy sum x < (2L + 1) q (c0 + L Shoup products, each in [0, 2q)):
+// log2 conditional subtractions instead of one per term (q < 2^60, L <= 7 keeps x < 16 q)
+template <int LT>
+__device__ __forceinline__ u64 reduce_lazy_sum(u64 x, u64 q) {
+  if constexpr (2 * LT + 1 > 8) x = csub(x, 8 * q);
+  if constexpr (2 * LT + 1 > 4) x = csub(x, 4 * q);
+  x = csub(x, 2 * q);
+  return csub(x, q);
+}
+
 // x in [0, 2^64): x mod q in [0, 2q)  (Shoup with w = 1)
 __device__ __forceinline__ u64 reduce_2q(u64 x, u64 one_sh, u64 q) { return x - __umul64hi(x, one_sh) * q; }
 

@@ -679,12 +679,12 @@ __global__ void __launch_bounds__(256, 2) ksmac_gemm_kernel(KsMacArgs a) {
         } else {
           const u64* kp = skey + (size_t)tap * 4 * NL * BNP + p_own;
 #pragma unroll
-          for (int i = 0; i < NL; i++) {
-            r0 = csub(r0 + shoup_mul(pre[h].d[i], kp[(4 * i) * BNP], kp[(4 * i + 1) * BNP], q), q2);
-            r1 = csub(r1 + shoup_mul(pre[h].d[i], kp[(4 * i + 2) * BNP], kp[(4 * i + 3) * BNP], q), q2);
+          for (int i = 0; i < NL; i++) {  // lazy sums, one canonical reduction each
+            r0 += shoup_mul(pre[h].d[i], kp[(4 * i) * BNP], kp[(4 * i + 1) * BNP], q);
+            r1 += shoup_mul(pre[h].d[i], kp[(4 * i + 2) * BNP], kp[(4 * i + 3) * BNP], q);
           }
-          r0 = csub(r0, q);  // canonical: the 30-bit split needs R < 2^60
-          r1 = csub(r1, q);
+          r0 = reduce_lazy_sum<NL>(r0, q);  // canonical: the 30-bit split needs R < 2^60
+          r1 = reduce_lazy_sum<NL>(r1, q);
         }
       }
       Rs[buf][kkl][0][p_own] = make_double2((double)(uint32_t)(r0 >> 30), (double)(uint32_t)(r0 & M30));
@@ -840,12 +840,12 @@ __global__ void __launch_bounds__(256) ksmac_thin_kernel(KsMacArgs a, int units)
           const u64 q = cst.q, q2 = cst.two_q;
           u64 x0 = c0v[u], x1 = 0;
 #pragma unroll
-          for (int i = 0; i < LT; i++) {
-            x0 = csub(x0 + shoup_mul(dv[u][i], kr.v[2 * i], kr.sh[2 * i], q), q2);
-            x1 = csub(x1 + shoup_mul(dv[u][i], kr.v[2 * i + 1], kr.sh[2 * i + 1], q), q2);
+          for (int i = 0; i < LT; i++) {  // lazy sums, one canonical reduction each
+            x0 += shoup_mul(dv[u][i], kr.v[2 * i], kr.sh[2 * i], q);
+            x1 += shoup_mul(dv[u][i], kr.v[2 * i + 1], kr.sh[2 * i + 1], q);
           }
-          r0 = csub(x0, q);  // canonical: the 30-bit split needs R < 2^60
-          r1 = csub(x1, q);
+          r0 = reduce_lazy_sum<LT>(x0, q);  // canonical: the 30-bit split needs R < 2^60
+          r1 = reduce_lazy_sum<LT>(x1, q);
         }
       } else {
         const u64* C0 = a.C0 + (size_t)z * LN;

@@ -148,3 +148,31 @@ def encrypt_sparse(P, s, slots, seed, nz=12):
         e = synth.cbd(synth.rng(seed, "e", 900 + j), P.N)
         out[j] = bfv.encrypt(P, m, s, a, e)
     return out
+
+
+@pytest.mark.parametrize("name", ["C3b", "C4"])
+def test_fullsize_host_pipeline_matches_device(hy, name):
+    """hy_conv_eval_host (uploads / downloads pipelined over batches of units on the library's
+    copy streams) returns exactly the device path's ciphertexts at full size."""
+    cfg = synth.configs()[name]
+    full = hy.hy_plan_layout(cfg.N, cfg.t, **cfg.shape_dict())
+    elts = list(full.galois[:full.n_galois])
+    ct = synth.gen_uniform_cts(cfg.primes, full.J, cfg.N, cfg.index, stream=3)
+    p = hy.hy_params_create(cfg.N, cfg.primes, cfg.t, 0)
+    try:
+        hy.hy_keys_upload(p, elts, synth.gen_uniform_keys(cfg.primes, len(elts), cfg.N, cfg.index))
+        w = hy.hy_encode_weights(p, synth.gen_weights(cfg), **cfg.shape_dict())
+        try:
+            lay = hy.hy_weights_layout(w)
+            d_out = torch.empty((lay.Jout, 2, len(cfg.primes), cfg.N), dtype=torch.uint64, device="cuda")
+            hy.hy_conv_eval(w, torch.from_numpy(ct).cuda(), d_out)
+            torch.cuda.synchronize()
+            dev = d_out.cpu().numpy()
+            del d_out
+            host = np.zeros_like(dev)
+            hy.hy_conv_eval_host(w, ct, host)
+            assert np.array_equal(host, dev)
+        finally:
+            hy.hy_weights_destroy(w)
+    finally:
+        hy.hy_params_destroy(p)

@@ -11,7 +11,7 @@ LIB = os.path.join(HERE, "libhyena.so")
 SOURCES = ["api.cu", "kernels.cu"]
 HEADERS = ["hy_common.cuh", "ntt.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177"]
+              "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177,128"]
 
 
 def _newest_input() -> float:

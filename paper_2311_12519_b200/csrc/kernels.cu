@@ -1400,7 +1400,10 @@ constexpr int KT_STAGE_A = KT_KS * 4096, KT_STAGE_B = KT_KS * 8 * 1024;
 constexpr size_t KT_SMEM_MMA = (size_t)KT_STAGES * (KT_STAGE_A + KT_STAGE_B) + 1024;
 inline size_t kt_smem(int T, int L) { return KT_SMEM_MMA + (size_t)T * 4 * L * TC_POS * sizeof(u64); }
 
-template <int LT, int LOGN>  // LOGN > 0: compile-time ring degree (address math folds into immediates)
+// LOGN > 0: compile-time ring degree (address math folds into immediates).  UNI: Jc % 4 == 0, so
+// every thread's 4-term group is one tap's consecutive cts, all real or all padding: only the
+// fast paths are compiled (fewer registers).
+template <int LT, int LOGN, bool UNI>
 __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, const int8_t* __restrict__ w8) {
   pdl_trigger();  // key staging and TMEM setup read only uploaded data: they overlap the predecessor
   extern __shared__ uint8_t kt_dyn[];
@@ -1455,7 +1458,16 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
     int tap = tap0, c = c0t;
     // common case: the thread's 4 terms share one tap (no ct wrap) and are all real terms: one
     // permutation and base address, strided loads, no per-term tests
-    grp = (c0t + 3 < a.Jcb && ch * KT_CHUNK + tg * 4 + 3 < a.K && !a.dbg) ? tap0 : -1;
+    if constexpr (UNI) {
+      grp = ch * KT_CHUNK + tg * 4 < a.K ? tap0 : -2;  // -2: a padding group (R = 0)
+      if (grp == -2) {
+#pragma unroll
+        for (int t = 0; t < 4; t++) pr[t].tap = -1;
+        return;
+      }
+    } else {
+      grp = (c0t + 3 < a.Jcb && ch * KT_CHUNK + tg * 4 + 3 < a.K && !a.dbg) ? tap0 : -1;
+    }
     if (grp >= 0 && a.coef) {  // 1x1 coefficient domain: R = the 4 input cts themselves
       const u64* ctp = a.C0 + ((size_t)z * a.Jcb + c) * 2 * LN + (size_t)l * N + j;
 #pragma unroll
@@ -1471,7 +1483,7 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
       }
       return;
     }
-    if (grp >= 0) {
+    if (UNI || grp >= 0) {
       const u64* C0 = C0u + (size_t)c * LN;
       const u64* D = Du + (size_t)c * (LT * LN);
       const bool ident = a.tt.key[tap] == nullptr;
@@ -1494,6 +1506,7 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
       }
       return;
     }
+    if constexpr (UNI) return;
 #pragma unroll
     for (int t = 0; t < 4; t++) {
       if (t > 0 && ++c >= a.Jcb) {
@@ -1598,7 +1611,18 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
     // R (byte planes), and the epilogue's single reduction makes the output canonical, so R
     // needs no reduction at all.
     uint32_t lo0[4], hi0[4], lo1[4], hi1[4];
-    if (grp >= 0 && s_haskey[grp]) {  // fast path: one tap, 4 real terms, keys at one address
+    if (UNI && grp < 0) {  // padding group
+#pragma unroll
+      for (int t = 0; t < 4; t++) lo0[t] = hi0[t] = lo1[t] = hi1[t] = 0;
+    } else if (UNI && !s_haskey[grp]) {  // identity tap
+#pragma unroll
+      for (int t = 0; t < 4; t++) {
+        lo0[t] = (uint32_t)cur[t].c0;
+        hi0[t] = (uint32_t)(cur[t].c0 >> 32);
+        lo1[t] = (uint32_t)cur[t].d[0];
+        hi1[t] = (uint32_t)(cur[t].d[0] >> 32);
+      }
+    } else if (UNI || (grp >= 0 && s_haskey[grp])) {  // fast path: one tap, 4 real terms, keys at one address
       const u64* kp = skey + (size_t)grp * 4 * LT * TC_POS + pos;
 #pragma unroll
       for (int t = 0; t < 4; t++) {
@@ -1613,7 +1637,7 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
         lo1[t] = (uint32_t)r1;
         hi1[t] = (uint32_t)(r1 >> 32);
       }
-    } else
+    } else if constexpr (!UNI)
 #pragma unroll
     for (int t = 0; t < 4; t++) {
       const int tap = cur[t].tap;
@@ -1716,17 +1740,17 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS));
 }
 
-template <int LT, int LOGN>
+template <int LT, int LOGN, bool UNI>
 hy_status launch_ksmac_tc_t(const KsMacArgs& a, const int8_t* w8, int units, cudaStream_t s) {
   const int N = 1 << a.logN;
   static bool attr_done = false;
   if (!attr_done) {
-    HY_CUDA_TRY(cudaFuncSetAttribute(ksmac_tc_kernel<LT, LOGN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    HY_CUDA_TRY(cudaFuncSetAttribute(ksmac_tc_kernel<LT, LOGN, UNI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kt_smem(HY_MAX_TAPS, LT)));
     attr_done = true;
   }
   dim3 grid((unsigned)(a.L * (N / TC_POS)), (unsigned)((a.Mpad + 127) / 128), (unsigned)units);
-  HY_CUDA_TRY(hy_launch(ksmac_tc_kernel<LT, LOGN>, grid, dim3(KT_THREADS), kt_smem(a.T, LT), s, 1, a, w8));
+  HY_CUDA_TRY(hy_launch(ksmac_tc_kernel<LT, LOGN, UNI>, grid, dim3(KT_THREADS), kt_smem(a.T, LT), s, 1, a, w8));
   HY_LAUNCH_CHECK();
   return HY_OK;
 }
@@ -1734,8 +1758,9 @@ hy_status launch_ksmac_tc_t(const KsMacArgs& a, const int8_t* w8, int units, cud
 // N = 8192 (the metric's ring degree) gets compile-time address math; other N the generic kernel
 template <int LT>
 hy_status launch_ksmac_tc(const KsMacArgs& a, const int8_t* w8, int units, cudaStream_t s) {
-  if (a.logN == 13) return launch_ksmac_tc_t<LT, 13>(a, w8, units, s);
-  return launch_ksmac_tc_t<LT, 0>(a, w8, units, s);
+  const bool uni = a.Jcb % 4 == 0 && a.K % 4 == 0 && !a.dbg;
+  if (a.logN == 13) return uni ? launch_ksmac_tc_t<LT, 13, true>(a, w8, units, s) : launch_ksmac_tc_t<LT, 13, false>(a, w8, units, s);
+  return uni ? launch_ksmac_tc_t<LT, 0, true>(a, w8, units, s) : launch_ksmac_tc_t<LT, 0, false>(a, w8, units, s);
 }
 
 hy_status launch_mac_tc(const KsMacArgs& a, const u64* R, const int8_t* w8, int units, cudaStream_t s) {

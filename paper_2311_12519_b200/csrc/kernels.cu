@@ -1549,11 +1549,15 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
     s_act[t] = a.tt.act[t];
   }
   // stage the key words of this CTA (limb l, positions j0 .. j0 + 15) for every tap
-  for (int e = tid; e < ((a.dbg & 16) ? 0 : a.T * 4 * LT * TC_POS); e += KT_THREADS) {
-    const int p = e % TC_POS, r = e / TC_POS;
+  // 16 consecutive words (128 B) per (tap, digit/component, value/Shoup) row: 16-byte loads
+  for (int e = tid; e < ((a.dbg & 16) ? 0 : a.T * 4 * LT * (TC_POS / 2)); e += KT_THREADS) {
+    const int p2 = e % (TC_POS / 2), r = e / (TC_POS / 2);
     const int sh = r % 2, x = (r / 2) % (2 * LT), tap = r / (4 * LT);
     const u64* key = a.tt.key[tap];
-    skey[e] = key ? __ldg(key + (size_t)sh * 2 * LT * LN + (size_t)x * LN + (size_t)l * N + j0 + p) : 0ull;
+    const ulonglong2 v = key ? __ldg(reinterpret_cast<const ulonglong2*>(key + (size_t)sh * 2 * LT * LN +
+                                                                          (size_t)x * LN + (size_t)l * N + j0) + p2)
+                             : make_ulonglong2(0ull, 0ull);
+    reinterpret_cast<ulonglong2*>(skey)[e] = v;
   }
   if (tid < KT_STAGES) s_ticket[tid] = 0;
   if (tid == 0) {

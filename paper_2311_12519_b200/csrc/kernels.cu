@@ -611,11 +611,14 @@ __global__ void __launch_bounds__(256, 2) ksmac_gemm_kernel(KsMacArgs a) {
     s_act[t] = a.tt.act[t];
   }
   if constexpr (LT > 0) {
-    for (int e = threadIdx.x; e < a.T * 4 * LT * BNP; e += 256) {
-      const int pp = e % BNP, r = e / BNP;
+    for (int e = threadIdx.x; e < a.T * 4 * LT * (BNP / 2); e += 256) {  // 16-byte loads
+      const int p2 = e % (BNP / 2), r = e / (BNP / 2);
       const int sh = r % 2, x = (r / 2) % (2 * LT), tap = r / (4 * LT);
       const u64* key = a.tt.key[tap];
-      skey[e] = key ? __ldg(key + (size_t)sh * 2 * LT * LNs + (size_t)x * LNs + (size_t)l * N + j0 + pp) : 0ull;
+      reinterpret_cast<ulonglong2*>(skey)[e] =
+          key ? __ldg(reinterpret_cast<const ulonglong2*>(key + (size_t)sh * 2 * LT * LNs + (size_t)x * LNs +
+                                                          (size_t)l * N + j0) + p2)
+              : make_ulonglong2(0ull, 0ull);
     }
   }
   __syncthreads();

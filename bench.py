@@ -1,12 +1,14 @@
 #!/usr/bin/env python
 """Benchmark of the Hyena encrypted-convolution hot path on B200 (contract: see DESIGN.md §Measurement).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
 
 A step = one hy_conv_eval of the configured layer (all of SURVEY §8(a): PermDecomp, PermAuto fused
 with the lazy MAC + WHT + reduction + sign PMult, row-swap alignment, INTT) on synthetic
-ciphertexts already resident in HBM.  Default workload: BASELINE.json configs[1] (C2,
-ResNet-20-style layer, N = 8192, L = 3), the configuration the metric is quoted on.
+ciphertexts already resident in HBM.  Default workload: BASELINE.json configs[3] (C4, the VGG-16
+early layer Ci = Co = 64 at 224 x 224, batch 8, N = 8192, L = 3): the metric names only N = 8192, so
+the workload is the largest single-GPU N = 8192 configuration; the other configs (--config) are
+parity-test cases and secondary lines.
 Multi-GPU (torchrun), --mode replica (default): every rank evaluates its own layer instance on
 its own images (weak scaling, no data-path collective); --mode shard: the ranks split ONE layer
 (units or output channels, paper_2311_12519_b200/shard.py) and rank 0 gathers the output
@@ -36,16 +38,22 @@ import synth
 
 METRIC = "encrypted conv layers/sec (ct×pt MAC GOps/s) at N=8192; % of HBM/INT roofline"
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+INT_PEAKS_PATH = os.path.join(ROOT, "profiles", "int_peaks.json")
 SM_COUNT = 148
 DFMA_PER_CLK_SM = 64     # FP64 pipe: 16 lanes/clk/SMSP x 4 (tools/intbench measured 58/clk/SM at 1965 MHz nominal)
 IMAD_PER_CLK_SM = 64
 
 
 def load_peaks():
-    try:
-        return json.load(open(PEAKS_PATH))
-    except Exception:
-        return {}
+    """MEASURED_PEAKS.json (driver-written: HBM copy GB/s, bf16 TF/s) + profiles/int_peaks.json
+    (tools/peaks.py on a B200: Shoup modmul, DFMA and tcgen05 int8 throughput)."""
+    out = {}
+    for path in (PEAKS_PATH, INT_PEAKS_PATH):
+        try:
+            out.update(json.load(open(path)))
+        except Exception:
+            pass
+    return out
 
 
 class ClockSampler:
@@ -140,9 +148,11 @@ def run_gpu(args, cfg, rank, world):
     if not empty:
         w = hy.hy_encode_weights(p, W, **shape)
         lay = hy.hy_weights_layout(w)
-        assert lay.J == len(ct_host)
+        # a units shard keeps the full layer's shape and evaluates its own units only
+        n_out = len(shard.out_index) if shard is not None else lay.Jout
+        assert len(ct_host) == n_out // lay.Jo * lay.Jc
         ct_in = torch.from_numpy(ct_host).to(device)
-        ct_out = torch.empty((lay.Jout, 2, L, cfg.N), dtype=torch.uint64, device=device)
+        ct_out = torch.empty((n_out, 2, L, cfg.N), dtype=torch.uint64, device=device)
     else:
         lay = None
         ct_out = torch.empty((0, 2, L, cfg.N), dtype=torch.uint64, device=device)
@@ -212,7 +222,7 @@ def run_gpu(args, cfg, rank, world):
     if w is not None:
         hy.hy_weights_set_stage_events(w, [])
         pin_in = torch.from_numpy(ct_host).pin_memory().numpy()
-        pin_out = torch.empty((lay.Jout, 2, L, cfg.N), dtype=torch.uint64).pin_memory().numpy()
+        pin_out = torch.empty(tuple(ct_out.shape), dtype=torch.uint64).pin_memory().numpy()
         for _ in range(2):
             hy.hy_conv_eval_host(w, pin_in, pin_out)
     torch.cuda.synchronize()
@@ -238,7 +248,7 @@ def run_gpu(args, cfg, rank, world):
                 stage_ms=[statistics.mean(s) if s else 0.0 for s in stage_ms],
                 mac_ms=statistics.mean(mac_ms) if mac_ms else 0.0, mac_launches=mac_n,
                 launches=launches, clocks=clk.summary(), lay=lay, full=full, e2e_s=e2e_s, e2e_steps=e2e_steps,
-                in_bytes=len(ct_host) * 2 * L * N * 8, out_bytes=(lay.Jout if lay else 0) * 2 * L * N * 8)
+                in_bytes=len(ct_host) * 2 * L * N * 8, out_bytes=int(ct_out.shape[0]) * 2 * L * N * 8)
 
 
 def layer_work(cfg, lay):
@@ -301,7 +311,9 @@ def roofline(cfg, res, peaks, steps):
     st = dict(zip(STAGES, res["stage_ms"]))
     path = res.get("mac_path", "tc_fused")
     clk_mhz = res["clocks"].get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
-    int_peak = MODMUL_PER_CLK_SM * SM_COUNT * clk_mhz * 1e6 / 1e9          # Gmodmul/s
+    mm_clk = peaks.get("modmul_per_clk_sm", MODMUL_PER_CLK_SM)            # measured (tools/peaks.py)
+    dfma_clk = peaks.get("dfma_per_clk_sm", DFMA_PER_CLK_SM)
+    int_peak = mm_clk * SM_COUNT * clk_mhz * 1e6 / 1e9                    # Gmodmul/s
     mac_ms = res["mac_ms"] or st["S2S3_ksmac_wht"]
     per_step = max(1, res["mac_launches"] // max(1, min(steps, 10)))
     dom = max(st, key=st.get)
@@ -328,14 +340,16 @@ def roofline(cfg, res, peaks, steps):
         a = (w["r_bytes"] + w["out_bytes"] * (2 if lay.cn == 2 and not cfg.depthwise else 1)) / (mac_ms * 1e-3) / 1e9
         mac = {"bound": "hbm", "achieved": a, "peak": hbm, "unit": "GB/s", "frac": a / hbm}
     else:
-        pk = DFMA_PER_CLK_SM * SM_COUNT * clk_mhz * 1e6 / 1e12
+        pk = dfma_clk * SM_COUNT * clk_mhz * 1e6 / 1e12
         a = w["dfma"] / (mac_ms * 1e-3) / 1e12
         mac = {"bound": "alu", "achieved": a, "peak": pk, "unit": "TDFMA/s", "frac": a / pk}
     mac.update(kernel=MAC_KERNEL[path], ms=mac_ms, launches_per_step=per_step)
     if path.startswith("tc"):
         i8 = 2 * 8 * w["coef_macs"] / (mac_ms * 1e-3) / 1e12                # 8 byte planes
-        i8_peak = peaks.get("bf16_tflops", 2250.0) * I8_PER_BF16
-        mac["tensor_int8"] = {"achieved": i8, "peak": i8_peak, "unit": "TOP/s", "frac": i8 / i8_peak}
+        i8_peak = peaks.get("i8_tensor_tops") or peaks.get("bf16_tflops", 2250.0) * I8_PER_BF16
+        mac["tensor_int8"] = {"achieved": i8, "peak": i8_peak, "unit": "TOP/s", "frac": i8 / i8_peak,
+                              "peak_source": "profiles/int_peaks.json (tcgen05 kind::i8 microbench)"
+                              if peaks.get("i8_tensor_tops") else "bf16 measured x nominal int8/bf16 ratio 2"}
     kernels["S2S3_ksmac_wht"] = mac
     top = dict(kernels[dom])
     top.setdefault("kernel", {"S1_permdecomp": "ntt_fwd_kernel<PermDecompJob> (S1)",
@@ -343,8 +357,9 @@ def roofline(cfg, res, peaks, steps):
     top["dominant_stage"] = dom
     top["share_of_step"] = st[dom] / max(1e-9, sum(st.values()))
     top["traffic"] = traffic_for(cfg.name, dom)
-    top["peak_note"] = (f"INT: {MODMUL_PER_CLK_SM:g} Shoup modmul/clk/SM x {SM_COUNT} SMs x {clk_mhz:.0f} MHz (derived "
-                        "from the unit counts, DESIGN.md §4); HBM: MEASURED_PEAKS.json hbm_gbs")
+    src = "measured, profiles/int_peaks.json" if "modmul_per_clk_sm" in peaks else "unit-count nominal"
+    top["peak_note"] = (f"INT: {mm_clk:g} Shoup modmul/clk/SM ({src}) x {SM_COUNT} SMs x {clk_mhz:.0f} MHz; "
+                        "HBM: MEASURED_PEAKS.json hbm_gbs")
     top["stages"] = kernels
     return top
 
@@ -352,69 +367,76 @@ def roofline(cfg, res, peaks, steps):
 # --------------------------------------------------------------------------------------------
 # CPU oracle (cpu_baseline leg and --impl reference)
 # --------------------------------------------------------------------------------------------
-def oracle_sample(cfg, budget_s: float = 20.0):
-    """Time the oracle as it stands on a bounded sample of the layer: one input ciphertext's
-    PermDecomp + one hoisted rotation, and one output group's MAC/WHT/sign/(row swap) — then
-    extrapolate linearly to the layer's rotation and output counts.  Returns (layers/s, desc)."""
+def oracle_sample(cfg):
+    """Time the oracle AS IT STANDS on a bounded, exact 1/J share of the layer (J = input cts):
+    its work is one PermDecomp + hoisted rotation per (input ct, non-identity tap) and one MAC
+    (+ WHT, sign PMult and row-swap HRot for c_n = 2) per output ct, identical for every input /
+    output ct, so the sample = one input ct's rotations (conv.rotations) + Jout/J output cts'
+    evaluation from those rotations (conv.he_conv with R given) is 1/J of a layer.
+    Returns (layers per sample, seconds, description)."""
     from oracle import bfv, conv
-    from oracle.params import galois_elt_for_step, rowswap_elt
     P = bfv.BFVParams(cfg.N, cfg.primes, cfg.t)
     p = conv.plan(cfg.N, cfg.batch, cfg.Ci, cfg.Co, cfg.H, cfg.W, cfg.kh, cfg.kw, cfg.pad, cfg.depthwise,
                   cfg.force_cn)
-    ls = conv.setup(p, cfg.t)
-    L = P.L
-    ct = synth.gen_uniform_cts(cfg.primes, 1, cfg.N, cfg.index)[0]
-    key = synth.gen_uniform_keys(cfg.primes, 1, cfg.N, cfg.index)[0]
-    step = next(s for _, _, s in p.taps if s % (cfg.N // 2))
-    g = galois_elt_for_step(cfg.N, step)
-    t0 = time.perf_counter()
-    d = bfv.decompose(P, ct)
-    bfv.rotate_hoisted(P, ct, d, g, key)
-    t_rot = time.perf_counter() - t0
-    # one output group's MAC over its K terms (uses the same ct for every term: timing only)
+    ls = conv.setup(p, cfg.t, cfg.k)
+    ct = synth.gen_uniform_cts(cfg.primes, 1, cfg.N, cfg.index, stream=9)
+    kk = synth.gen_uniform_keys(cfg.primes, max(1, len(ls.galois)), cfg.N, cfg.index)
+    keys = {g: kk[n] for n, g in enumerate(ls.galois)}
     W = synth.gen_weights(cfg)
-    T = len(p.taps)
-    K = T if cfg.depthwise else p.Jc * T
+    n_out = max(1, p.Jout // p.J)
     t0 = time.perf_counter()
-    nB = 1 if p.cn == 1 else (2 if cfg.depthwise else 4)
-    for _ in range(nB):
-        conv._lincomb(P, [(int(W.flat[i % W.size]) or 1, ct) for i in range(K)])
-    if p.cn == 2:
-        from oracle import ring
-        S = conv.sign_poly(P, ls)
-        for _ in range(1 if cfg.depthwise else 2):
-            for comp in range(2):
-                for l, q in enumerate(P.primes):
-                    ring.nc_mul(S[l], ct[comp, l], q)
-    t_mac = time.perf_counter() - t0
-    n_rot = p.J * sum(1 for _, _, s in p.taps if s % (cfg.N // 2))
-    n_swap = p.Jout if (p.cn == 2 and not cfg.depthwise) else 0
-    n_groups = p.Jout
-    t_layer = (n_rot + n_swap) * t_rot + n_groups * t_mac
-    desc = (f"1 hoisted rotation ({t_rot:.2f} s) + 1 output group's MAC/WHT/sign ({t_mac:.2f} s), "
-            f"extrapolated x{n_rot + n_swap} rotations and x{n_groups} groups; single thread")
-    return 1.0 / t_layer, desc, t_rot + t_mac
+    R1 = conv.rotations(P, p, ct, keys, cts=[0])                  # one input ct, every tap
+    # every output ct of unit 0 reads R[(c, tau)] for all its input cts: the same rotated ct
+    # stands in for each (values do not change the oracle's work)
+    R = {(c, tau): R1[(0, tau)] for c in range(max(p.Jc, n_out)) for tau in range(len(p.taps))}
+    conv.he_conv(P, ls, W, ct, keys, out_cts=list(range(n_out)), R=R)
+    dt = time.perf_counter() - t0
+    n_rot = sum(1 for _, _, s in p.taps if s % (cfg.N // 2))
+    desc = (f"exact 1/J = 1/{p.J} share of the layer: 1 input ct's PermDecomp + {n_rot} hoisted rotations and "
+            f"{n_out} output ct(s)' MAC over {p.Jc if not p.depthwise else 1}x{len(p.taps)} terms"
+            + (" + WHT/sign PMult/row-swap HRot" if p.cn == 2 else "") + f" ({dt:.2f} s); single thread")
+    return 1.0 / p.J, dt, desc
 
 
 def run_reference(args, cfg):
-    import torch
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
-    samples, desc = [], ""
+    secs, desc, frac = [], "", 1.0
     for i in range(args.warmup + args.steps):
-        v, desc, _ = oracle_sample(cfg)
+        frac, dt, desc = oracle_sample(cfg)
         if i >= args.warmup:
-            samples.append(v)
-    v = statistics.median(samples)
+            secs.append(dt)
+    sec = sum(secs)
+    v = frac * len(secs) / sec
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "layers/s",
             "n_gpus": int(os.environ.get("WORLD_SIZE", 1)), "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": 1e3 * sec / len(secs), "layers_per_step": frac, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
             "dtype": "int (Python/NumPy + C schoolbook)", "data": "synthetic",
-            "config": {"workload": cfg.name, "N": cfg.N, "L": len(cfg.primes)},
-            "cpu_baseline": {"value": v, "unit": "layers/s", "cores": 1, "kind": "oracle", "sample": desc},
+            "config": {"workload": workload_name(cfg), "N": cfg.N, "L": len(cfg.primes)},
+            "cpu_baseline": {"value": v, "unit": "layers/s", "cores": 1, "kind": "oracle", "sample": desc,
+                             "host": host_info()},
             "e2e": {"value": v, "unit": "layers/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def host_info():
+    import platform
+    model = platform.processor()
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count()}
+
+
+def workload_name(cfg):
+    return (f"{cfg.name}: Ci={cfg.Ci} Co={cfg.Co} H=W={cfg.H} {cfg.kh}x{cfg.kw} pad={cfg.pad} batch={cfg.batch} "
+            f"depthwise={cfg.depthwise} N={cfg.N} L={len(cfg.primes)} (BASELINE.json configs)")
 
 
 # --------------------------------------------------------------------------------------------
@@ -423,7 +445,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="hyena", choices=["hyena", "reference"])
     ap.add_argument("--mode", default="replica", choices=["replica", "shard"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -458,8 +480,7 @@ def main():
             "dtype": "u64",
             "data": "synthetic (uniform ciphertexts + keys: RLWE-indistinguishable from real encryptions; "
                     "int8 weights uniform in the config's range)",
-            "config": {"workload": f"{cfg.name}: Ci={cfg.Ci} Co={cfg.Co} H=W={cfg.H} {cfg.kh}x{cfg.kw} pad={cfg.pad} "
-                                   f"batch={cfg.batch} depthwise={cfg.depthwise} (BASELINE.json configs)",
+            "config": {"workload": workload_name(cfg),
                        "N": cfg.N, "L": len(cfg.primes), "t": cfg.t, "c_n": full.cn, "k": full.k, "J": full.J,
                        "Jout": full.Jout, "rotations": work["rotations"], "rowswaps": work["rowswaps"],
                        "l2": "flushed between timed steps (256 MiB write, untimed)",
@@ -475,8 +496,9 @@ def main():
                     "d2h_bytes_per_step": res["out_bytes"]},
         }
         if world == 1 and not args.no_cpu_baseline:
-            v, desc, _ = oracle_sample(cfg)
-            line["cpu_baseline"] = {"value": v, "unit": "layers/s", "cores": 1, "kind": "oracle", "sample": desc}
+            frac, dt, desc = oracle_sample(cfg)
+            line["cpu_baseline"] = {"value": frac / dt, "unit": "layers/s", "cores": 1, "kind": "oracle",
+                                    "sample": desc, "host": host_info()}
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -25,7 +25,22 @@ void hy_set_error(const char* fmt, ...) {
 extern "C" const char* hy_last_error(void) { return g_err; }
 
 #include <atomic>
+#include <mutex>
 static std::atomic<uint64_t> g_launches{0};
+
+cudaError_t hy_smem_attr(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;  // (kernel, device) -> bytes set
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[std::make_pair(kernel, dev)];
+  if (have >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
 void hy_count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 extern "C" uint64_t hy_kernel_launches(void) { return g_launches.load(); }
 
@@ -381,22 +396,28 @@ extern "C" hy_status hy_keys_upload(hy_params* p, uint32_t n, const uint32_t* el
       hy_set_error("key copy: %s", cudaGetErrorString(ce));
       return HY_ECUDA;
     }
-    KeyEntry& ke = p->keys[g];
-    ke.g = g;
-    if (!ke.ntt) {
-      ce = cudaMalloc(&ke.ntt, 2 * key_words * sizeof(u64));
-      if (ce != cudaSuccess) {
-        p->keys.erase(g);
-        cudaFree(tmp);
-        hy_set_error("key alloc: %s", cudaGetErrorString(ce));
-        return HY_ENOMEM;
-      }
-    }
-    hy_status st = hyk::key_to_ntt(p, tmp, ke.ntt, 0);
-    if (st != HY_OK) {
+    // a replaced key is written into a FRESH buffer and swapped in only after the device is idle:
+    // an evaluation already queued on another stream keeps reading the old, complete key
+    u64* fresh = nullptr;
+    ce = cudaMalloc(&fresh, 2 * key_words * sizeof(u64));
+    if (ce != cudaSuccess) {
       cudaFree(tmp);
+      p->keys_version++;  // earlier elements of this call may have been replaced
+      hy_set_error("key alloc: %s", cudaGetErrorString(ce));
+      return HY_ENOMEM;
+    }
+    hy_status st = hyk::key_to_ntt(p, tmp, fresh, 0);
+    if (st == HY_OK) st = cudaDeviceSynchronize() == cudaSuccess ? HY_OK : HY_ECUDA;
+    if (st != HY_OK) {
+      cudaFree(fresh);
+      cudaFree(tmp);
+      p->keys_version++;
       return st;
     }
+    KeyEntry& ke = p->keys[g];
+    ke.g = g;
+    cudaFree(ke.ntt);  // device idle (synchronised above): nothing reads the old key any more
+    ke.ntt = fresh;
   }
   cudaError_t ce = cudaDeviceSynchronize();
   cudaFree(tmp);
@@ -505,7 +526,13 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
       hy_weights_destroy(w);
       return st;
     }
-    cudaMalloc(&w->d_sign, 2 * L * N * sizeof(u64));
+    if (cudaMalloc(&w->d_sign, 2 * L * N * sizeof(u64)) != cudaSuccess) {
+      w->d_sign = nullptr;
+      cudaFree(tmp);
+      hy_weights_destroy(w);
+      hy_set_error("sign plaintext allocation failed");
+      return HY_ENOMEM;
+    }
     st = hyk::ntt_poly_fwd(p, tmp, w->d_sign, 1, 0);
     if (st == HY_OK) st = hyk::shoup_table(p, w->d_sign, w->d_sign + L * N, 1, 0);
     cudaDeviceSynchronize();
@@ -547,10 +574,15 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
       return HY_ENOMEM;
     }
   }
-  HY_CUDA_TRY(cudaMalloc(&w->d_tap_keys, T * sizeof(u64*)));
-  HY_CUDA_TRY(cudaMalloc(&w->d_tap_act, T * sizeof(GaloisAct)));
+  cudaError_t ce = cudaMalloc(&w->d_tap_keys, T * sizeof(u64*));
+  if (ce == cudaSuccess) ce = cudaMalloc(&w->d_tap_act, T * sizeof(GaloisAct));
+  if (ce == cudaSuccess) ce = cudaDeviceSynchronize();
+  if (ce != cudaSuccess) {
+    hy_weights_destroy(w);
+    hy_set_error("hy_encode_weights: %s", cudaGetErrorString(ce));
+    return HY_ECUDA;
+  }
   w->keys_version = ~0ull;
-  HY_CUDA_TRY(cudaDeviceSynchronize());
   *out = w;
   return HY_OK;
 }
@@ -607,15 +639,19 @@ extern "C" hy_status hy_weights_set_mac_path(hy_weights* w, int32_t path) {
       hy_set_error("coefficient-domain workspace allocation failed");
       return HY_ENOMEM;
     }
-    if (Jo > Jin) {
-      cudaFree(w->d_D);
-      cudaFree(w->d_C0);
-      w->d_D = w->d_C0 = nullptr;
-      if (cudaMalloc(&w->d_D, Jo * L * L * N * sizeof(u64)) != cudaSuccess ||
-          cudaMalloc(&w->d_C0, Jo * L * N * sizeof(u64)) != cudaSuccess) {
+    if (Jo > Jin) {  // allocate the larger digit workspaces first: on failure the old ones stay valid
+      u64 *nd = nullptr, *nc = nullptr;
+      if (cudaMalloc(&nd, Jo * L * L * N * sizeof(u64)) != cudaSuccess ||
+          cudaMalloc(&nc, Jo * L * N * sizeof(u64)) != cudaSuccess) {
+        cudaFree(nd);
         hy_set_error("coefficient-domain digit workspace allocation failed");
         return HY_ENOMEM;
       }
+      cudaDeviceSynchronize();  // no evaluation may still read the old workspaces
+      cudaFree(w->d_D);
+      cudaFree(w->d_C0);
+      w->d_D = nd;
+      w->d_C0 = nc;
     }
   }
   const bool split = path == HY_MAC_TC_SPLIT || path == HY_MAC_FP64_SPLIT;

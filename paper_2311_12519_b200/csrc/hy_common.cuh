@@ -185,6 +185,10 @@ __device__ __forceinline__ void pdl_begin() {
   pdl_wait();
 }
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is a per-device-context attribute: set it once per
+// (kernel, device) to at least `bytes` (thread-safe; api.cu keeps the cache behind a mutex)
+cudaError_t hy_smem_attr(const void* kernel, size_t bytes);
+
 // launch with cudaLaunchAttributeProgrammaticStreamSerialization (optionally in clusters of cx)
 template <typename... KArgs, typename... Args>
 inline cudaError_t hy_launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cx,

@@ -314,11 +314,7 @@ hy_status launch_fwd_t(const hy_params* p, const Job& job, size_t npoly, cudaStr
   if (npoly == 0) return HY_OK;
   using C = NttCfg<LOGN>;
   const size_t sm = ntt_smem_bytes<LOGN>();
-  static bool attr_done = false;
-  if (!attr_done) {
-    HY_CUDA_TRY(cudaFuncSetAttribute(ntt_fwd_kernel<LOGN, Job>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr_done = true;
-  }
+  HY_CUDA_TRY(hy_smem_attr((const void*)ntt_fwd_kernel<LOGN, Job>, sm));
   HY_CUDA_TRY(hy_launch(ntt_fwd_kernel<LOGN, Job>, dim3((unsigned)(npoly * C::S)), dim3(C::T), sm, s, 1, job, p->tab,
                         limb_consts(p)));
   HY_LAUNCH_CHECK();
@@ -330,11 +326,7 @@ hy_status launch_inv_t(const hy_params* p, const Job& job, size_t npoly, cudaStr
   if (npoly == 0) return HY_OK;
   using C = NttCfg<LOGN>;
   const size_t sm = ntt_smem_bytes<LOGN>();
-  static bool attr_done = false;
-  if (!attr_done) {
-    HY_CUDA_TRY(cudaFuncSetAttribute(ntt_inv_kernel<LOGN, Job>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr_done = true;
-  }
+  HY_CUDA_TRY(hy_smem_attr((const void*)ntt_inv_kernel<LOGN, Job>, sm));
   HY_CUDA_TRY(hy_launch(ntt_inv_kernel<LOGN, Job>, dim3((unsigned)(npoly * C::S)), dim3(C::T), sm, s, C::S, job,
                         p->tab, limb_consts(p)));
   HY_LAUNCH_CHECK();
@@ -1688,6 +1680,9 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) {
+      // the ticket atomic is the thread synchronisation between successive UMMA issuers: order
+      // this thread's earlier tcgen05 ops (its last issue + commit) before it
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __threadfence_block();
       const int prev = atomicAdd(&s_ticket[s], 1);  // monotonic: use u of stage s takes tickets
       if (prev % KT_WARPS == KT_WARPS - 1) {       // 8u .. 8u + 7; the last warp issues the UMMAs
@@ -1750,12 +1745,7 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
 template <int LT, int LOGN, bool UNI>
 hy_status launch_ksmac_tc_t(const KsMacArgs& a, const int8_t* w8, int units, cudaStream_t s) {
   const int N = 1 << a.logN;
-  static bool attr_done = false;
-  if (!attr_done) {
-    HY_CUDA_TRY(cudaFuncSetAttribute(ksmac_tc_kernel<LT, LOGN, UNI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)kt_smem(HY_MAX_TAPS, LT)));
-    attr_done = true;
-  }
+  HY_CUDA_TRY(hy_smem_attr((const void*)ksmac_tc_kernel<LT, LOGN, UNI>, kt_smem(HY_MAX_TAPS, LT)));
   dim3 grid((unsigned)(a.L * (N / TC_POS)), (unsigned)((a.Mpad + 127) / 128), (unsigned)units);
   HY_CUDA_TRY(hy_launch(ksmac_tc_kernel<LT, LOGN, UNI>, grid, dim3(KT_THREADS), kt_smem(a.T, LT), s, 1, a, w8));
   HY_LAUNCH_CHECK();
@@ -1782,11 +1772,7 @@ template <int WM>
 hy_status launch_mac_gemm(const KsMacArgs& a, const u64* R, int units, cudaStream_t s) {
   using TL = MgTile<WM>;
   const int N = 1 << a.logN;
-  static bool attr_done = false;
-  if (!attr_done) {
-    HY_CUDA_TRY(cudaFuncSetAttribute(mac_gemm_kernel<WM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TL::SMEM));
-    attr_done = true;
-  }
+  HY_CUDA_TRY(hy_smem_attr((const void*)mac_gemm_kernel<WM>, TL::SMEM));
   dim3 grid((unsigned)(a.L * (N / TL::BNP)), (unsigned)(a.Mpad / TL::BM), (unsigned)units);
   mac_gemm_kernel<WM><<<grid, 256, TL::SMEM, s>>>(a, R);
   HY_LAUNCH_CHECK();
@@ -1807,11 +1793,7 @@ hy_status launch_ksmac_gemm_t(const KsMacArgs& a, int units, cudaStream_t s) {
   const int N = 1 << a.logN, BNP = 256 / WM, KC = 2 * WM;
   const size_t sm0 = sizeof(double2) * 2 * KC * 2 * BNP + sizeof(double) * 2 * KC * 8 * WM;
   const size_t sm = sm0 + (LT > 0 ? (size_t)a.T * 4 * LT * BNP * sizeof(u64) : 0);
-  static size_t attr = 0;
-  if (sm > attr) {
-    HY_CUDA_TRY(cudaFuncSetAttribute(ksmac_gemm_kernel<WM, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    attr = sm;
-  }
+  HY_CUDA_TRY(hy_smem_attr((const void*)ksmac_gemm_kernel<WM, LT>, sm));
   dim3 grid((unsigned)(a.L * (N / BNP)), (unsigned)(a.Mpad / (8 * WM)), (unsigned)units);
   HY_CUDA_TRY(hy_launch(ksmac_gemm_kernel<WM, LT>, grid, dim3(256), sm, s, 1, a));
   HY_LAUNCH_CHECK();

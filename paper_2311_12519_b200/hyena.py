@@ -188,16 +188,31 @@ def hy_weights_destroy(w: int):
     load_library().hy_weights_destroy(w)
 
 
+def _ct_words(w: int, shape, what: str) -> int:
+    """Words of a [n][2][L][N] ciphertext array for the weights' ring (checked shape)."""
+    lay = hy_weights_layout(w)
+    if len(shape) != 4 or tuple(shape[1:]) != (2, lay.L, lay.N):
+        raise HyenaError(f"{what}: expected shape [n][2][{lay.L}][{lay.N}], got {tuple(shape)}")
+    return int(shape[0]) * 2 * lay.L * lay.N
+
+
 def hy_conv_eval(w: int, ct_in, ct_out, J: Optional[int] = None, Jout: Optional[int] = None, stream=None):
     J = ct_in.shape[0] if J is None else J
     Jout = ct_out.shape[0] if Jout is None else Jout
-    _check(load_library().hy_conv_eval(w, _dev_ptr(ct_in), J, _dev_ptr(ct_out), Jout, _stream(stream)),
+    wi, wo = _ct_words(w, ct_in.shape, "ct_in"), _ct_words(w, ct_out.shape, "ct_out")
+    if J > ct_in.shape[0] or Jout > ct_out.shape[0]:
+        raise HyenaError("J / Jout exceed the buffers")
+    _check(load_library().hy_conv_eval(w, _dev_ptr(ct_in, wi), J, _dev_ptr(ct_out, wo), Jout, _stream(stream)),
            "hy_conv_eval")
 
 
 def hy_conv_eval_host(w: int, ct_in: np.ndarray, ct_out: np.ndarray, stream=None):
-    assert ct_in.dtype == np.uint64 and ct_out.dtype == np.uint64
-    assert ct_in.flags.c_contiguous and ct_out.flags.c_contiguous
+    if not (ct_in.dtype == np.uint64 and ct_out.dtype == np.uint64):
+        raise HyenaError("host ciphertexts must be uint64")
+    if not (ct_in.flags.c_contiguous and ct_out.flags.c_contiguous):
+        raise HyenaError("host ciphertexts must be C-contiguous")
+    _ct_words(w, ct_in.shape, "ct_in")
+    _ct_words(w, ct_out.shape, "ct_out")
     _check(load_library().hy_conv_eval_host(w, ct_in.ctypes.data, ct_in.shape[0], ct_out.ctypes.data,
                                             ct_out.shape[0], _stream(stream)), "hy_conv_eval_host")
 

@@ -108,10 +108,68 @@ __global__ void k_shoup(const int32_t* __restrict__ w, int64_t* out, int n) {
   if (s == 0x123456789) out[0] = s;
 }
 
+// tcgen05 int8 tensor-core throughput (the roofline of the byte-plane MAC's tensor side): one CTA
+// per SM, one thread issues back-to-back kind::i8 UMMAs M=128 N=256 K=32 (the MAC kernels' shape)
+// from fixed shared-memory tiles into one TMEM accumulator, then waits on the commit.
+#define MMA_ITERS 8192
+__global__ void __launch_bounds__(128) k_umma_i8(const int32_t* __restrict__ w, int64_t* out, int n) {
+  __shared__ __align__(1024) uint8_t sA[128 * 32];
+  __shared__ __align__(1024) uint8_t sB[256 * 32];
+  __shared__ uint32_t s_tmem;
+  __shared__ __align__(8) uint64_t mbar;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int e = tid; e < 128 * 32; e += 128) sA[e] = (uint8_t)(e * 37 + w[e & 31]);
+  for (int e = tid; e < 256 * 32; e += 128) sB[e] = (uint8_t)(e * 91 + 3);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_tmem)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  const uint32_t mb = (uint32_t)__cvta_generic_to_shared(&mbar);
+  if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = s_tmem;
+  auto desc = [](uint32_t saddr) {
+    uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)(128 >> 4) << 16;
+    d |= (uint64_t)(256 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+  };
+  if (tid == 0) {
+    const uint32_t id = (2u << 4) | (1u << 7) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint64_t da = desc((uint32_t)__cvta_generic_to_shared(sA)), db = desc((uint32_t)__cvta_generic_to_shared(sB));
+    for (int it = 0; it < MMA_ITERS; it++)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+          "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+          "l"(da), "l"(db), "r"(id), "r"(it));
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mb) : "memory");
+  }
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(mb), "r"(0));
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  uint32_t r0;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r0) : "r"(tmem + ((uint32_t)(warp * 32) << 16)));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  if (r0 == 0x12345u) out[0] = r0;
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
+}
+
 typedef void (*kfn)(const int32_t*, int64_t*, int);
 
-static void run(const char* name, kfn f, double ops_per_inner, int* w, int64_t* o) {
-  int sms = 148, blocks = sms * 8, threads = 256;
+static void run(const char* name, kfn f, double ops_per_inner, int* w, int64_t* o, int blocks = 148 * 8,
+                int threads = 256, double ops_per_thread = 0) {
+  int sms = 148;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -123,7 +181,8 @@ static void run(const char* name, kfn f, double ops_per_inner, int* w, int64_t* 
   cudaEventSynchronize(e1);
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
-  double ops = (double)blocks * threads * ITERS * 8 * ops_per_inner * reps;
+  double ops = ops_per_thread > 0 ? (double)blocks * ops_per_thread * reps
+                                 : (double)blocks * threads * ITERS * 8 * ops_per_inner * reps;
   int clk_khz;
   cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
   double per_s = ops / (ms * 1e-3);
@@ -143,6 +202,8 @@ int main() {
   run("dfma", k_dfma, 1, w, o);
   run("shoup_modmul64", k_shoup, 1, w, o);
   run("iadd_xor_shift(3 ops)", k_iadd3, 3, w, o);
+  // per CTA: MMA_ITERS UMMAs of 2 * 128 * 256 * 32 int8 ops
+  run("tcgen05_i8_ops", k_umma_i8, 0, w, o, 148, 128, (double)MMA_ITERS * 2 * 128 * 256 * 32);
   cudaError_t e = cudaDeviceSynchronize();
   printf("status %s\n", cudaGetErrorString(e));
   return 0;

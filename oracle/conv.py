@@ -276,7 +276,9 @@ def _lincomb(P: bfv.BFVParams, terms) -> np.ndarray:
         for l, q in enumerate(P.primes):
             hi = np.zeros(N, dtype=np.int64)
             lo = np.zeros(N, dtype=np.int64)
-            for w, c in terms:       # exact: |w| <= 2^8, digits < 2^30, <= 2^20 terms
+            # exact in int64: |w| <= 2^13 (Hadamard scalars k (w0 + w1), k <= 32), 30-bit digits,
+            # <= 2^16 terms (the planner's bound): |sum| < 2^59
+            for w, c in terms:
                 v = c[comp, l]
                 hi += w * (v >> np.uint64(30)).astype(np.int64)
                 lo += w * (v & np.uint64((1 << 30) - 1)).astype(np.int64)
@@ -344,30 +346,34 @@ def he_conv(P: bfv.BFVParams, ls: LayerSetup, Wt: np.ndarray, ct_in: np.ndarray,
                     terms.append((_weight(Wt, p, go, c, tau), R[(u * p.Jc + c, tau)]))
             res[oc] = _lincomb(P, terms)
             continue
-        # c_n = 2: diagonals d (reading R15): slot row r of diagonal d pairs input channel
-        # 2j+r with output channel 2g+(r xor d)
+        # c_n = 2, ProposedConv of Algorithm 1 (PAPER.md:1530-1551 [ign]) per diagonal d (reading
+        # R15: slot row r of diagonal d pairs input channel 2j+r with output channel 2g+(r xor d)):
+        # the Hadamard filter scalars of (j, tau) are the slot-row weights w_r pushed through the
+        # Walsh-Hadamard rows of Eq. (2) ([k, -k] for [1, -1]):
+        #   row 0 ([1, 1], the constant plaintext 1):   k (w_0 + w_1)
+        #   row 1 ([k, -k], the sign plaintext S):        w_0 - w_1
+        # lazily multiplied with the rotated ct and accumulated into partial sum (row, g), then
+        # each partial sum is reduced ONCE, multiplied by its Hadamard-row plaintext, and the rows
+        # are added (Algorithm).
         diags = [0] if p.depthwise else [0, 1]
         Pd = []
         for d in diags:
-            B = []
-            for r in range(2):
-                terms = []
-                js = [go] if p.depthwise else range(p.Jc)
-                for j in js:
-                    for tau in range(T):
-                        w = _weight(Wt, p, 2 * go + (r ^ d), 2 * j + r, tau)
-                        terms.append((w, R[(u * p.Jc + j, tau)]))
-                B.append(_lincomb(P, terms))
-            # Walsh-Hadamard (Eq. 2): A0 = k (B0 + B1), A1 = B0 - B1, then PMult by [k, -k]
+            terms = ([], [])
+            js = [go] if p.depthwise else range(p.Jc)
+            for j in js:
+                for tau in range(T):
+                    w0 = _weight(Wt, p, 2 * go + (0 ^ d), 2 * j + 0, tau)
+                    w1 = _weight(Wt, p, 2 * go + (1 ^ d), 2 * j + 1, tau)
+                    Rjt = R[(u * p.Jc + j, tau)]
+                    terms[0].append((ls.k * (w0 + w1), Rjt))
+                    terms[1].append((w0 - w1, Rjt))
+            A0 = _lincomb(P, terms[0])          # reduced partial sum of Hadamard row 0
+            A1 = _lincomb(P, terms[1])          # reduced partial sum of Hadamard row 1
             part = np.empty((2, P.L, P.N), dtype=np.uint64)
             for comp in range(2):
                 for l, q in enumerate(P.primes):
-                    b0 = B[0][comp, l].astype(object)
-                    b1 = B[1][comp, l].astype(object)
-                    a0 = (ls.k * (b0 + b1)) % q
-                    a1 = ((b0 - b1) % q).astype(np.uint64)
-                    sa1 = ring.nc_mul(S[l], a1, q).astype(object)
-                    part[comp, l] = ((a0 + sa1) % q).astype(np.uint64)
+                    sa1 = ring.nc_mul(S[l], A1[comp, l], q).astype(object)   # PMult by [k, -k]
+                    part[comp, l] = ((A0[comp, l].astype(object) + sa1) % q).astype(np.uint64)   # HAdd
             Pd.append(part)
         if p.depthwise:
             res[oc] = Pd[0]

@@ -562,8 +562,6 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
       {&w->d_A1, (lay.cn == 2 && w->mac_path == HY_MAC_TC_COEF) ? Jo * 2 * ctw : 0},
       {&w->d_R, (w->mac_path == HY_MAC_TC_SPLIT || w->mac_path == HY_MAC_FP64_SPLIT)
                     ? (size_t)w->r_units * w->K * ctw : 0},
-      {&w->d_in, Jin * ctw},
-      {&w->d_out, Jo * ctw},
   };
   for (auto& a : allocs) {
     if (!a.words) continue;
@@ -787,6 +785,16 @@ extern "C" hy_status hy_conv_eval_host(hy_weights* w, const uint64_t* in, size_t
   HY_CHECK(nu <= lay.U && Jout == nu * lay.Jo, HY_ESHAPE, "J=%zu / Jout=%zu do not match the layout", J, Jout);
   HY_CUDA_TRY(cudaSetDevice(w->p->device));
   cudaStream_t s = (cudaStream_t)stream;
+  if (!w->d_in) {  // staging buffers of the host path: allocated on first use
+    const size_t Jin = (size_t)lay.U * lay.Jc, Jo = (size_t)lay.U * lay.Jo;
+    if (cudaMalloc(&w->d_in, Jin * ctw * sizeof(u64)) != cudaSuccess ||
+        cudaMalloc(&w->d_out, Jo * ctw * sizeof(u64)) != cudaSuccess) {
+      cudaFree(w->d_in);
+      w->d_in = w->d_out = nullptr;
+      hy_set_error("host-path staging allocation failed");
+      return HY_ENOMEM;
+    }
+  }
   if (!w->s_h2d) {
     HY_CUDA_TRY(cudaStreamCreateWithFlags(&w->s_h2d, cudaStreamNonBlocking));
     HY_CUDA_TRY(cudaStreamCreateWithFlags(&w->s_d2h, cudaStreamNonBlocking));

@@ -96,10 +96,12 @@ def test_fullsize_ciphertext_parity(hy, name):
     assert (got < q).all()
 
 
-@pytest.mark.parametrize("name", ["C2", "C3a", "C3b", "C4", "C5dw_8192"])
+@pytest.mark.parametrize("name", FULL)
 def test_fullsize_decrypts_to_plain_conv(hy, name):
-    """Real BFV encryptions (sparse masks a) of the sampled units' inputs, uniform junk
-    elsewhere: the sampled outputs decrypt to scale * conv mod t at every valid position."""
+    """Real BFV encryptions (DENSE uniform masks a, CBD errors, dense Galois keys: the real
+    noise of the key switching) of the sampled units' inputs, uniform junk elsewhere: the
+    sampled outputs decrypt to scale * conv mod t at every valid position, and the noise meter
+    (SURVEY §5, P12; PAPER.md:266-267 [ign], :318) shows >= 4 bits of margin below Delta/2."""
     cfg = synth.configs()[name]
     P = bfv.BFVParams(cfg.N, cfg.primes, cfg.t)
     plan = conv.plan(cfg.N, cfg.batch, cfg.Ci, cfg.Co, cfg.H, cfg.W, cfg.kh, cfg.kw, cfg.pad, cfg.depthwise,
@@ -115,8 +117,7 @@ def test_fullsize_decrypts_to_plain_conv(hy, name):
     if plan.depthwise:          # a depthwise output reads only its own channel
         need = sorted({oc // plan.Jo * plan.Jc + oc % plan.Jo for oc in outs})
     ct_in = sparse_c1_cts(cfg.primes, plan.J, cfg.N, cfg.index + 50)
-    enc = encrypt_sparse(P, s, slots[need], cfg.index)
-    ct_in[need] = enc
+    ct_in[need] = encrypt_slots(P, s, slots[need], cfg.index)
     keys = keygen(P, s, ls.galois, cfg.index)
     got, lay = run_full(hy, cfg, ct_in, keys)
     dec = conv.decrypt_outputs(P, ls, {oc: got[oc] for oc in outs}, s)
@@ -131,6 +132,11 @@ def test_fullsize_decrypts_to_plain_conv(hy, name):
     assert have.sum() > 0
     bad = np.argwhere(have & (got_px != exp))
     assert bad.size == 0, f"{name}: {len(bad)} mismatches, first {bad[:5].tolist()}"
+    budget = bfv.noise_budget_bits(P)
+    margins = {oc: budget - bfv.noise_bits(P, got[oc], s, bfv.decrypt(P, got[oc], s)) for oc in outs}
+    print(f"{name}: noise margin bits (log2(Delta/2) - log2 ||v||) = "
+          + ", ".join(f"ct {oc}: {m:.1f}" for oc, m in margins.items()))
+    assert min(margins.values()) >= 4, f"{name}: noise margin {margins}"
 
 
 def encrypt_sparse(P, s, slots, seed, nz=12):

@@ -185,6 +185,25 @@ hy_status hy_weights_set_mac_path(hy_weights* w, int32_t path);
 hy_status hy_decrypt_debug(const hy_params* p, const int8_t* sk, const uint64_t* ct, size_t n, uint32_t scale,
                            uint64_t* slots_out);
 
+/* Client-side draws on the GPU (symmetric BFV encryption PAPER.md:242-253
+ * [\ignore], keys of reading R5).  Every random number comes from Philox4x32-10 keyed by `seed`, with
+ * the counter layout and value mappings documented in synth/philox.py (ternary secret, centered
+ * binomial eta = 20 errors, uniform masks), so the CPU oracle reproduces each call bit for bit.
+ * All three synchronise the device and allocate their own scratch.
+ * hy_secret_key: the ternary secret s of `seed`, host int8 [N] (for hy_decrypt_debug).
+ * hy_keygen:     switching keys for n Galois elements (odd, < 2N), [n][L digits][2: b, a][L limbs][N]
+ *                coefficient form: b_{i,l} = [-a_{i,l} s + e_i + [i == l] s(X^g)]_{q_l}.  keys_out: device
+ *                buffer or NULL; upload != 0 also installs them (hy_keys_upload).
+ * hy_encrypt:    ct_j = ([Delta m_j + a_j s + e_j]_{q_l}, [-a_j]_{q_l}), Delta = floor(Q/t), for the n
+ *                plaintexts m (host [n][N], coefficients in [0, t)) with encryption counters
+ *                first .. first + n - 1; ct_out device [n][2][L][N] coefficient form.
+ * Errors: HY_EINVAL (bad element / coefficient), HY_ENOMEM, HY_ECUDA. */
+hy_status hy_secret_key(const hy_params* p, uint64_t seed, int8_t* sk_out);
+hy_status hy_keygen(hy_params* p, uint64_t seed, uint32_t n, const uint32_t* galois_elts, uint64_t* keys_out,
+                    int upload);
+hy_status hy_encrypt(const hy_params* p, uint64_t seed, const uint64_t* m, size_t n, uint32_t first,
+                     uint64_t* ct_out, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

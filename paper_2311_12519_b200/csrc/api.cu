@@ -314,6 +314,8 @@ extern "C" hy_status hy_params_create(uint32_t N, const uint64_t* q, uint32_t L,
     c.c32 = (1ull << 32) % ql;
     c.c32_sh = shoup(c.c32, ql);
     c.off62 = ql * (((1ull << 62) + ql - 1) / ql);
+    c.c64 = (u64)(((u128)1 << 64) % ql);
+    c.c64_sh = shoup(c.c64, ql);
   }
   // slot-order position j <-> bit-reversed butterfly position k, split into the
   // NTT blocks of HY_NTT_BLOCK coefficients
@@ -334,6 +336,16 @@ extern "C" hy_status hy_params_create(uint32_t N, const uint64_t* q, uint32_t L,
           own_k.push_back((int32_t)(kos[j] - h * B));
         }
   }
+  std::vector<u64> psi2((size_t)2 * L * N), ipsi2((size_t)2 * L * N);
+  for (uint32_t l = 0; l < L; l++)
+    for (uint32_t k = 0; k < N; k++) {
+      const size_t i = (size_t)l * N + k;
+      psi2[2 * i] = k ? psi_rev[i] : 0;
+      psi2[2 * i + 1] = k ? psi_rev_sh[i] : 0;
+      const u64 iw = k ? ipsi_rev[i] : mulmod(ipsi_rev[(size_t)l * N + 1], p->lc[l].ninv, q[l]);
+      ipsi2[2 * i] = iw;
+      ipsi2[2 * i + 1] = shoup(iw, q[l]);
+    }
   const size_t bytes = (size_t)L * N * sizeof(u64);
   hy_status st;
   if ((st = upload((void**)&p->tab.psi_rev, psi_rev.data(), bytes)) != HY_OK ||
@@ -341,7 +353,10 @@ extern "C" hy_status hy_params_create(uint32_t N, const uint64_t* q, uint32_t L,
       (st = upload((void**)&p->tab.ipsi_rev, ipsi_rev.data(), bytes)) != HY_OK ||
       (st = upload((void**)&p->tab.ipsi_rev_sh, ipsi_rev_sh.data(), bytes)) != HY_OK ||
       (st = upload((void**)&p->tab.own_j, own_j.data(), N * sizeof(int32_t))) != HY_OK ||
-      (st = upload((void**)&p->tab.own_k, own_k.data(), N * sizeof(int32_t))) != HY_OK) {
+      (st = upload((void**)&p->tab.own_k, own_k.data(), N * sizeof(int32_t))) != HY_OK ||
+      (st = upload((void**)&p->tab.psi2, psi2.data(), 2 * bytes)) != HY_OK ||
+      (st = upload((void**)&p->tab.ipsi2, ipsi2.data(), 2 * bytes)) != HY_OK ||
+      (st = upload((void**)&p->tab.kos, kos.data(), N * sizeof(int32_t))) != HY_OK) {
     hy_params_destroy(p);
     return st;
   }
@@ -364,6 +379,9 @@ extern "C" void hy_params_destroy(hy_params* p) {
   cudaFree(p->tab.ipsi_rev_sh);
   cudaFree(p->tab.own_j);
   cudaFree(p->tab.own_k);
+  cudaFree(p->tab.psi2);
+  cudaFree(p->tab.ipsi2);
+  cudaFree(p->tab.kos);
   for (auto& kv : p->keys) cudaFree(kv.second.ntt);
   delete p;
 }
@@ -399,7 +417,7 @@ extern "C" hy_status hy_keys_upload(hy_params* p, uint32_t n, const uint32_t* el
     // a replaced key is written into a FRESH buffer and swapped in only after the device is idle:
     // an evaluation already queued on another stream keeps reading the old, complete key
     u64* fresh = nullptr;
-    ce = cudaMalloc(&fresh, 2 * key_words * sizeof(u64));
+    ce = cudaMalloc(&fresh, 3 * key_words * sizeof(u64));
     if (ce != cudaSuccess) {
       cudaFree(tmp);
       p->keys_version++;  // earlier elements of this call may have been replaced
@@ -878,6 +896,92 @@ extern "C" hy_status hy_rotate(hy_params* p, const uint64_t* ct_in, uint32_t g, 
   cudaFree(work);
   if (st != HY_OK) return st;
   HY_CHECK(ce == cudaSuccess, HY_ECUDA, "%s", cudaGetErrorString(ce));
+  return HY_OK;
+}
+
+// ============================================================================================
+// client-side draws on the GPU: Philox4x32-10, counter layout of
+// synth/philox.py; the oracle-side client reproduces every draw bit for bit
+// ============================================================================================
+namespace {
+struct DevBuf {  // RAII device allocation for the synchronous client calls
+  void* p = nullptr;
+  ~DevBuf() { cudaFree(p); }
+};
+}  // namespace
+
+extern "C" hy_status hy_secret_key(const hy_params* p, uint64_t seed, int8_t* sk_out) {
+  HY_CHECK(p && sk_out, HY_EINVAL, "null argument");
+  HY_CUDA_TRY(cudaSetDevice(p->device));
+  const size_t L = p->L, N = p->N;
+  DevBuf sres, s8;
+  HY_CUDA_TRY(cudaMalloc(&sres.p, L * N * 8));
+  HY_CUDA_TRY(cudaMalloc(&s8.p, N));
+  HY_TRY(hyk::client_secret(p, seed, (int8_t*)s8.p, (u64*)sres.p, nullptr, 0));
+  HY_CUDA_TRY(cudaMemcpy(sk_out, s8.p, N, cudaMemcpyDeviceToHost));
+  return HY_OK;
+}
+
+extern "C" hy_status hy_keygen(hy_params* p, uint64_t seed, uint32_t n, const uint32_t* elts, uint64_t* keys_out,
+                               int upload) {
+  HY_CHECK(p && (n == 0 || elts), HY_EINVAL, "null argument");
+  if (n == 0) return HY_OK;
+  for (uint32_t e = 0; e < n; e++)
+    HY_CHECK((elts[e] & 1) && elts[e] < 2 * p->N, HY_EINVAL, "Galois element %u must be odd and < 2N", elts[e]);
+  HY_CUDA_TRY(cudaSetDevice(p->device));
+  const size_t L = p->L, N = p->N, kw = L * 2 * L * N;
+  DevBuf sres, s8, sntt, del, work, kout;
+  HY_CUDA_TRY(cudaMalloc(&sres.p, L * N * 8));
+  HY_CUDA_TRY(cudaMalloc(&s8.p, N));
+  HY_CUDA_TRY(cudaMalloc(&sntt.p, 2 * L * N * 8));
+  HY_CUDA_TRY(cudaMalloc(&del.p, n * sizeof(uint32_t)));
+  HY_CUDA_TRY(cudaMemcpy(del.p, elts, n * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  // work: A, NTT(A) [n L][L][N], s(X^g) [n][L][N], errors [n L][N] int32
+  HY_CUDA_TRY(cudaMalloc(&work.p, (2 * n * L * L * N + n * L * N) * 8 + n * L * N * 4));
+  u64* out = keys_out;
+  if (!out) {
+    HY_CUDA_TRY(cudaMalloc(&kout.p, n * kw * 8));
+    out = (u64*)kout.p;
+  }
+  HY_TRY(hyk::client_secret(p, seed, (int8_t*)s8.p, (u64*)sres.p, (u64*)sntt.p, 0));
+  HY_TRY(hyk::client_keygen(p, seed, (const u64*)sntt.p, (const int8_t*)s8.p, (const uint32_t*)del.p, n, out,
+                            (u64*)work.p, 0));
+  HY_CUDA_TRY(cudaDeviceSynchronize());
+  if (upload) HY_TRY(hy_keys_upload(p, n, elts, out, 1));
+  return HY_OK;
+}
+
+extern "C" hy_status hy_encrypt(const hy_params* p, uint64_t seed, const uint64_t* m, size_t n, uint32_t first,
+                                uint64_t* ct_out, void* stream) {
+  HY_CHECK(p && m && ct_out, HY_EINVAL, "null argument");
+  if (n == 0) return HY_OK;
+  HY_CUDA_TRY(cudaSetDevice(p->device));
+  const size_t L = p->L, N = p->N;
+  // Delta = floor(Q / t) mod q_l = -(Q mod t) t^{-1} mod q_l  (Q = 0 mod q_l)
+  u64 r = 1;
+  for (size_t l = 0; l < L; l++) r = mulmod(r, p->q[l] % p->t, p->t);
+  u64 delta[HY_MAX_LIMBS];
+  for (size_t l = 0; l < L; l++) {
+    const u64 q = p->q[l];
+    delta[l] = mulmod((q - r % q) % q, invmod(p->t % q, q), q);
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  DevBuf sres, s8, sntt, md, idx, work;
+  HY_CUDA_TRY(cudaMalloc(&sres.p, L * N * 8));
+  HY_CUDA_TRY(cudaMalloc(&s8.p, N));
+  HY_CUDA_TRY(cudaMalloc(&sntt.p, 2 * L * N * 8));
+  HY_CUDA_TRY(cudaMalloc(&md.p, n * N * 8));
+  HY_CUDA_TRY(cudaMalloc(&idx.p, n * sizeof(uint32_t)));
+  HY_CUDA_TRY(cudaMalloc(&work.p, 2 * n * L * N * 8 + n * N * 4));
+  std::vector<uint32_t> ids(n);
+  for (size_t o = 0; o < n; o++) ids[o] = first + (uint32_t)o;
+  for (size_t i = 0; i < n * N; i++) HY_CHECK(m[i] < p->t, HY_EINVAL, "plaintext coefficient %zu not < t", i);
+  HY_CUDA_TRY(cudaMemcpyAsync(md.p, m, n * N * 8, cudaMemcpyHostToDevice, st));
+  HY_CUDA_TRY(cudaMemcpyAsync(idx.p, ids.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+  HY_TRY(hyk::client_secret(p, seed, (int8_t*)s8.p, (u64*)sres.p, (u64*)sntt.p, st));
+  HY_TRY(hyk::client_encrypt(p, seed, (const u64*)sntt.p, (const u64*)md.p, (const uint32_t*)idx.p, n, delta, ct_out,
+                             (u64*)work.p, st));
+  HY_CUDA_TRY(cudaStreamSynchronize(st));
   return HY_OK;
 }
 

@@ -57,6 +57,7 @@ struct LimbConst {
   u64 off;                // q * ceil(2^59 / q): makes |x| < 2^59 signed values nonnegative
   u64 c32, c32_sh;        // 2^32 mod q and Shoup companion (tensor-core MAC epilogue)
   u64 off62;              // q * ceil(2^62 / q): makes |x| < 2^62 signed values nonnegative
+  u64 c64, c64_sh;        // 2^64 mod q and Shoup companion (16-plane MAC epilogue)
 };
 
 struct DevTables {
@@ -71,6 +72,12 @@ struct DevTables {
   // forward transform leaves at butterfly position bitrev((e_j - 1)/2).
   int32_t* own_j;
   int32_t* own_k;
+  // one-CTA NTT (ntt2_*, N = 4096 / 8192): interleaved (w, w') [L][N] for psi / psi^{-1} (entry 0 of
+  // the inverse table = psi^{-bitrev(1)} N^{-1}, the last inverse stage with the scaling folded in),
+  // and kos[j] = butterfly position of slot j
+  ulonglong2* psi2;
+  ulonglong2* ipsi2;
+  int32_t* kos;
 };
 
 // Galois automorphism X -> X^g, g = (+/-) 3^shift mod 2N, acting on slot-ordered NTT vectors:
@@ -85,7 +92,8 @@ struct GaloisAct {
 
 struct KeyEntry {
   uint32_t g;
-  u64* ntt;  // device [L digits][2][L limbs][N] values, then the same again for Shoup companions
+  u64* ntt;  // device [L digits][2][L limbs][N] values, then the same again for Shoup companions, then
+            // the same again with each value w split into 30-bit halves (w mod 2^30) | (w >> 30) << 32
 };
 
 struct hy_params {
@@ -274,4 +282,9 @@ hy_status rotate_ct(const hy_params* p, const u64* ct_in, GaloisAct act, const u
                     u64* work, cudaStream_t s);
 hy_status decrypt_phase(const hy_params* p, const u64* s_ntt, const u64* s_ntt_sh, const u64* ct, size_t n,
                         u64* x_out, u64* work, cudaStream_t st);
+hy_status client_secret(const hy_params* p, u64 seed, int8_t* sk8_dev, u64* s_res, u64* s_ntt, cudaStream_t st);
+hy_status client_encrypt(const hy_params* p, u64 seed, const u64* s_ntt, const u64* m_dev, const uint32_t* idx_dev,
+                         size_t n, const u64* delta_l, u64* ct_out, u64* work, cudaStream_t st);
+hy_status client_keygen(const hy_params* p, u64 seed, const u64* s_ntt, const int8_t* sk8_dev, const uint32_t* elts_dev,
+                        size_t n_elts, u64* keys_out, u64* work, cudaStream_t st);
 }  // namespace hyk

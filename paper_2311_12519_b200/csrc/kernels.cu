@@ -333,8 +333,41 @@ hy_status launch_inv_t(const hy_params* p, const Job& job, size_t npoly, cudaStr
   return HY_OK;
 }
 
+// one-CTA-per-transform NTT (ntt2_*) for N = 4096 / 8192 when the launch has enough transforms to
+// fill the GPU (throughput); small launches keep the split kernels (half the latency of one
+// transform: the latency-bound small layers).  HY_NTT_V1 forces the split kernels (A/B).
+constexpr size_t NTT2_MIN_POLYS = 148 * 4;
+static bool ntt_v1() {
+  static const bool v = getenv("HY_NTT_V1") != nullptr;
+  return v;
+}
+
+template <int LOGN, class Job>
+hy_status launch_fwd2_t(const hy_params* p, const Job& job, size_t npoly, cudaStream_t s) {
+  if (npoly == 0) return HY_OK;
+  const size_t sm = ntt2_smem_bytes<LOGN>();
+  HY_CUDA_TRY(hy_smem_attr((const void*)ntt2_fwd_kernel<LOGN, Job>, sm));
+  HY_CUDA_TRY(hy_launch(ntt2_fwd_kernel<LOGN, Job>, dim3((unsigned)npoly), dim3(Ntt2Cfg<LOGN>::T), sm, s, 1, job,
+                        Ntt2Tables{p->tab.psi2, p->tab.kos}, limb_consts(p)));
+  HY_LAUNCH_CHECK();
+  return HY_OK;
+}
+
+template <int LOGN, class Job>
+hy_status launch_inv2_t(const hy_params* p, const Job& job, size_t npoly, cudaStream_t s) {
+  if (npoly == 0) return HY_OK;
+  const size_t sm = ntt2_smem_bytes<LOGN>();
+  HY_CUDA_TRY(hy_smem_attr((const void*)ntt2_inv_kernel<LOGN, Job>, sm));
+  HY_CUDA_TRY(hy_launch(ntt2_inv_kernel<LOGN, Job>, dim3((unsigned)npoly), dim3(Ntt2Cfg<LOGN>::T), sm, s, 1, job,
+                        Ntt2Tables{p->tab.ipsi2, p->tab.kos}, limb_consts(p)));
+  HY_LAUNCH_CHECK();
+  return HY_OK;
+}
+
 template <class Job>
 hy_status launch_fwd(const hy_params* p, const Job& job, size_t nblocks, cudaStream_t s) {
+  if (!ntt_v1() && nblocks >= NTT2_MIN_POLYS && p->logN == 13) return launch_fwd2_t<13>(p, job, nblocks, s);
+  if (!ntt_v1() && nblocks >= NTT2_MIN_POLYS && p->logN == 12) return launch_fwd2_t<12>(p, job, nblocks, s);
   switch (p->logN) {
     case 10: return launch_fwd_t<10>(p, job, nblocks, s);
     case 11: return launch_fwd_t<11>(p, job, nblocks, s);
@@ -348,6 +381,8 @@ hy_status launch_fwd(const hy_params* p, const Job& job, size_t nblocks, cudaStr
 
 template <class Job>
 hy_status launch_inv(const hy_params* p, const Job& job, size_t nblocks, cudaStream_t s) {
+  if (!ntt_v1() && nblocks >= NTT2_MIN_POLYS && p->logN == 13) return launch_inv2_t<13>(p, job, nblocks, s);
+  if (!ntt_v1() && nblocks >= NTT2_MIN_POLYS && p->logN == 12) return launch_inv2_t<12>(p, job, nblocks, s);
   switch (p->logN) {
     case 10: return launch_inv_t<10>(p, job, nblocks, s);
     case 11: return launch_inv_t<11>(p, job, nblocks, s);
@@ -368,6 +403,14 @@ __global__ void shoup_table_kernel(const u64* __restrict__ w, u64* __restrict__ 
     const int l = (int)((i / N) % L);
     const u64 q = qa.q[l];
     wsh[i] = (u64)(((u128)w[i] << 64) / q);
+  }
+}
+
+// w (< 2^60) -> (w mod 2^30) | (w >> 30) << 32: the operand form of the exact 30-bit-split products
+__global__ void split30_kernel(const u64* __restrict__ w, u64* __restrict__ out, size_t total) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const u64 x = w[i];
+    out[i] = (x & 0x3FFFFFFFull) | ((x >> 30) << 32);
   }
 }
 
@@ -1742,6 +1785,41 @@ __global__ void __launch_bounds__(KT_THREADS, 2) ksmac_tc_kernel(KsMacArgs a, co
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TC_TMEM_COLS));
 }
 
+#include "ksmac_v2.cuh"
+
+template <int LT, int LOGN, int EPI>
+hy_status launch_ksmac_v2_t(const KsMacArgs& a, const int8_t* w8, int units, const V2Geom& g, cudaStream_t s) {
+  int dev = 0, nsm = 148;
+  HY_CUDA_TRY(cudaGetDevice(&dev));
+  HY_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  const int ntiles = units * a.L * ((1 << a.logN) / TC_POS);
+  HY_CUDA_TRY(hy_smem_attr((const void*)ksmac_v2_kernel<LT, LOGN, EPI>, g.bytes));
+  HY_CUDA_TRY(hy_launch(ksmac_v2_kernel<LT, LOGN, EPI>, dim3((unsigned)std::min(ntiles, nsm)),
+                        dim3(V2Warps<EPI>::THREADS), g.bytes, s, 1, a, w8, g, units));
+  HY_LAUNCH_CHECK();
+  return HY_OK;
+}
+
+#include "ksmac_v3.cuh"
+
+template <int LT, int LOGN, int EPI>
+hy_status launch_ksmac_v3_t(const KsMacArgs& a, const int8_t* w8, int units, const V2Geom& g, cudaStream_t s) {
+  int dev = 0, nsm = 148;
+  HY_CUDA_TRY(cudaGetDevice(&dev));
+  HY_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+  const int ntiles = units * a.L * ((1 << a.logN) / V3_POS);
+  HY_CUDA_TRY(hy_smem_attr((const void*)ksmac_v3_kernel<LT, LOGN, EPI>, g.bytes));
+  HY_CUDA_TRY(hy_launch(ksmac_v3_kernel<LT, LOGN, EPI>, dim3((unsigned)std::min(ntiles, nsm)),
+                        dim3(V2Warps<EPI>::THREADS), g.bytes, s, 1, a, w8, g, units));
+  HY_LAUNCH_CHECK();
+  return HY_OK;
+}
+
+template <int LT, int LOGN>
+hy_status launch_ksmac_v2(const KsMacArgs& a, const int8_t* w8, int units, const V2Geom& g, cudaStream_t s) {
+  return a.M <= 64 ? launch_ksmac_v2_t<LT, LOGN, 2>(a, w8, units, g, s) : launch_ksmac_v2_t<LT, LOGN, 4>(a, w8, units, g, s);
+}
+
 template <int LT, int LOGN, bool UNI>
 hy_status launch_ksmac_tc_t(const KsMacArgs& a, const int8_t* w8, int units, cudaStream_t s) {
   const int N = 1 << a.logN;
@@ -1756,6 +1834,24 @@ hy_status launch_ksmac_tc_t(const KsMacArgs& a, const int8_t* w8, int units, cud
 template <int LT>
 hy_status launch_ksmac_tc(const KsMacArgs& a, const int8_t* w8, int units, cudaStream_t s) {
   const bool uni = a.Jcb % 4 == 0 && a.K % 4 == 0 && !a.dbg;
+  // HY_KSMAC=1: the non-persistent Shoup-producer kernel, 2: the persistent Shoup-producer kernel,
+  // default (3): the persistent exact-product kernel (A/B measurements)
+  static const int ver = getenv("HY_KSMAC") ? atoi(getenv("HY_KSMAC")) : 3;
+  if (uni && !a.coef && ver == 3 && a.Mpad <= 128 && a.wblocks == 1) {
+    const V2Geom g = v3_geom(a.T, LT, a.Kpad, 232448);
+    if (g.S >= 2) {
+      if (a.logN == 13)
+        return a.M <= 64 ? launch_ksmac_v3_t<LT, 13, 2>(a, w8, units, g, s) : launch_ksmac_v3_t<LT, 13, 4>(a, w8, units, g, s);
+      return a.M <= 64 ? launch_ksmac_v3_t<LT, 0, 2>(a, w8, units, g, s) : launch_ksmac_v3_t<LT, 0, 4>(a, w8, units, g, s);
+    }
+  }
+  if (uni && !a.coef && ver == 2 && a.Mpad <= 128 && a.wblocks == 1) {
+    const V2Geom g = v2_geom(a.T, LT, a.Kpad, 232448);
+    if (g.S >= 2) {
+      if (a.logN == 13) return launch_ksmac_v2<LT, 13>(a, w8, units, g, s);
+      return launch_ksmac_v2<LT, 0>(a, w8, units, g, s);
+    }
+  }
   if (a.logN == 13) return uni ? launch_ksmac_tc_t<LT, 13, true>(a, w8, units, s) : launch_ksmac_tc_t<LT, 13, false>(a, w8, units, s);
   return uni ? launch_ksmac_tc_t<LT, 0, true>(a, w8, units, s) : launch_ksmac_tc_t<LT, 0, false>(a, w8, units, s);
 }
@@ -1833,6 +1929,163 @@ hy_status launch_ksmac(const KsMacArgs& a, int tile, int units, cudaStream_t s) 
   return HY_EINVAL;
 }
 
+// ------------------------------------------------------------------------------------------
+// Client-side draws on the GPU (hy_secret_key / hy_keygen / hy_encrypt):
+// Philox4x32-10 with the counter layout and the value mappings of synth/philox.py, which the
+// oracle-side client reimplements in NumPy (bit-identical draws; tests/test_gpu_client.py).
+// ------------------------------------------------------------------------------------------
+struct Philox4 {
+  uint32_t x[4];
+};
+__device__ __forceinline__ Philox4 philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint64_t seed) {
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    if (r) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  return Philox4{{c0, c1, c2, c3}};
+}
+// floor(X q / 2^128), X = the 128-bit block
+__device__ __forceinline__ u64 philox_uniform(const Philox4& b, u64 q) {
+  const u64 xlo = (u64)b.x[0] | ((u64)b.x[1] << 32), xhi = (u64)b.x[2] | ((u64)b.x[3] << 32);
+  const u64 a1 = __umul64hi(xhi, q), a0 = xhi * q, b1 = __umul64hi(xlo, q);
+  const u64 s = a0 + b1;
+  return a1 + (s < a0 ? 1ull : 0ull);
+}
+__device__ __forceinline__ int philox_ternary(const Philox4& b) {
+  const u64 y = (u64)b.x[0] | ((u64)b.x[1] << 32);
+  return (int)__umul64hi(y, 3ull) - 1;
+}
+__device__ __forceinline__ int philox_cbd20(const Philox4& b) {
+  const u64 y = (u64)b.x[0] | ((u64)b.x[1] << 32);
+  return __popcll(y & 0xFFFFFull) - __popcll((y >> 20) & 0xFFFFFull);
+}
+
+// secret s (ternary) lifted into every limb: out [L][N]
+__global__ void gen_secret_kernel(u64 seed, int L, int logN, QArr qa, u64* __restrict__ s_res, int8_t* __restrict__ s8) {
+  const int N = 1 << logN;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+    const int v = philox_ternary(philox4x32_10((uint32_t)k, 0u, 0u, 1u, seed));
+    if (s8) s8[k] = (int8_t)v;
+    for (int l = 0; l < L; l++) s_res[(size_t)l * N + k] = v >= 0 ? (u64)v : qa.q[l] - 1;
+  }
+}
+
+// masks: uniform residues [n][L][N] with counter (k, c1 = base1 + o, c2 = base2 + l (key: 256 i + l), purpose)
+struct MaskArgs {
+  u64 seed;
+  uint32_t purpose;
+  int L, logN;
+  size_t n;
+  const uint32_t* c1;   // per poly-group o: counter word 1 (encryption index or Galois element)
+  uint32_t c2_mul;      // key masks: group o = (element, digit i): c2 = 256 i + l; encryption: c2 = l
+  QArr qa;
+};
+__global__ void gen_mask_kernel(MaskArgs m, u64* __restrict__ out) {
+  const int N = 1 << m.logN;
+  const size_t total = m.n * m.L * (size_t)N;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+    const int k = (int)(idx & (N - 1));
+    const size_t ol = idx >> m.logN;
+    const int l = (int)(ol % m.L);
+    const size_t o = ol / m.L;
+    uint32_t c1, c2;
+    if (m.c2_mul) {  // key: o = element index * L + digit
+      c1 = m.c1[o / m.L];
+      c2 = 256u * (uint32_t)(o % m.L) + (uint32_t)l;
+    } else {
+      c1 = m.c1[o];
+      c2 = (uint32_t)l;
+    }
+    out[idx] = philox_uniform(philox4x32_10((uint32_t)k, c1, c2, m.purpose, m.seed), m.qa.q[l]);
+  }
+}
+// errors: centered binomial [n][N] (int32), counter (k, c1, c2 = 256 i for keys / 0, purpose)
+__global__ void gen_error_kernel(u64 seed, uint32_t purpose, int logN, size_t n, const uint32_t* __restrict__ c1v,
+                                 int digits, int32_t* __restrict__ out) {
+  const int N = 1 << logN;
+  const size_t total = n * (size_t)N;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+    const int k = (int)(idx & (N - 1));
+    const size_t o = idx >> logN;
+    const uint32_t c1 = digits ? c1v[o / digits] : c1v[o];
+    const uint32_t c2 = digits ? 256u * (uint32_t)(o % digits) : 0u;
+    out[idx] = philox_cbd20(philox4x32_10((uint32_t)k, c1, c2, purpose, seed));
+  }
+}
+
+// c = INTT(NTT(a) .* NTT(s)) and the client's combination, per (poly o, limb):
+//   encryption: c0 = [Delta m + a s + e], c1 = [-a]           (symmetric BFV)
+//   key digit i: b = [-a s + e_i + [i == l] s(X^g)], a kept  (reading R5, RNS-digit gadget)
+struct ClientInvJob {
+  const u64* An;        // [n][L][N] NTT(a)
+  const u64* Sn;        // [L][N] NTT(s), then [L][N] Shoup companions
+  const u64* A;         // [n][L][N] a (coefficient form)
+  const int32_t* E;     // [n][N] errors
+  const u64* M;         // encryption: [n][N] plaintext coefficients (< t); keys: null
+  const u64* Sg;        // keys: [n_elts][L][N] s(X^g) lifted per limb; encryption: null
+  u64* out;             // [n][2][L][N]
+  int L, N, digits;     // digits = L for keys (o = element * L + i), 0 for encryption
+  QArr qa, delta;       // delta: Delta mod q_l
+  int limb, o;
+  __device__ void bind(int b) {
+    o = b / L;
+    limb = b % L;
+  }
+  __device__ u64 load(int k) const {
+    const size_t at = ((size_t)o * L + limb) * N + k;
+    const u64 q = qa.q[limb];
+    return csub(shoup_mul(An[at], Sn[(size_t)limb * N + k], Sn[(size_t)(L + limb) * N + k], q), q);
+  }
+  __device__ void store(int k, u64 as) const {
+    const u64 q = qa.q[limb];
+    const size_t at = ((size_t)o * L + limb) * N + k;
+    const int32_t e = E[(size_t)o * N + k];
+    const u64 er = e >= 0 ? (u64)e : q - (u64)(-e);
+    u64* c = out + (size_t)o * 2 * L * N;
+    if (!digits) {
+      const u64 dm = mulmod_slow(delta.q[limb], M[(size_t)o * N + k], q);
+      c[(size_t)limb * N + k] = csub(csub(csub(dm + as, q) + er, q), q);
+      c[(size_t)(L + limb) * N + k] = A[at] ? q - A[at] : 0;
+    } else {
+      const int i = o % digits;
+      u64 b = csub((as ? q - as : 0) + er, q);
+      if (i == limb) b = csub(b + Sg[((size_t)(o / digits) * L + limb) * N + k], q);
+      c[(size_t)limb * N + k] = b;
+      c[(size_t)(L + limb) * N + k] = A[at];
+    }
+  }
+};
+
+// s(X^g) coefficient form, lifted per limb: sg[l][(k g) mod N] = +/- s[k]
+__global__ void automorph_secret_kernel(const int8_t* __restrict__ s8, const uint32_t* __restrict__ elts, int n_elts,
+                                        int L, int logN, QArr qa, u64* __restrict__ sg) {
+  const int N = 1 << logN;
+  const size_t total = (size_t)n_elts * N;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+    const int k = (int)(idx & (N - 1));
+    const int e = (int)(idx >> logN);
+    const u64 pos = ((u64)k * elts[e]) % (2 * (u64)N);
+    int v = s8[k];
+    int at = (int)pos;
+    if (pos >= (u64)N) {
+      at -= N;
+      v = -v;
+    }
+    for (int l = 0; l < L; l++) sg[((size_t)e * L + l) * N + at] = v >= 0 ? (u64)v : qa.q[l] - (u64)(-v);
+  }
+}
+
 }  // namespace
 
 // ============================================================================================
@@ -1864,10 +2117,16 @@ hy_status shoup_table(const hy_params* p, const u64* w, u64* wsh, size_t npoly, 
 }
 
 hy_status key_to_ntt(const hy_params* p, const u64* key_coeff, u64* key_ntt, cudaStream_t s) {
-  // key [L][2][L][N] -> NTT per (digit, comp, limb); Shoup companions in the following block
+  // key [L][2][L][N] -> NTT per (digit, comp, limb); Shoup companions in the following block, then
+  // the 30-bit split values (the exact-product MAC producers, ksmac_v3)
   const size_t npoly = 2 * p->L;  // groups of L limbs
+  const size_t words = npoly * p->L * p->N;
   HY_TRY(ntt_poly_fwd(p, key_coeff, key_ntt, npoly, s));
-  return shoup_table(p, key_ntt, key_ntt + npoly * p->L * p->N, npoly, s);
+  HY_TRY(shoup_table(p, key_ntt, key_ntt + words, npoly, s));
+  split30_kernel<<<(unsigned)std::min<size_t>((words + 255) / 256, 148 * 16), 256, 0, s>>>(key_ntt, key_ntt + 2 * words,
+                                                                                           words);
+  HY_LAUNCH_CHECK();
+  return HY_OK;
 }
 
 hy_status permdecomp(const hy_params* p, const u64* ct, size_t nct, u64* D, u64* C0, cudaStream_t s) {
@@ -2158,6 +2417,56 @@ hy_status rotate_ct(const hy_params* p, const u64* ct_in, GaloisAct act, const u
   HY_TRY(launch_ks_apply(ka, s));
   OutInvJob jx{X, 2 * L * N, ct_out, (int)L, (int)N};
   return launch_inv(p, jx, n * 2 * L, s);
+}
+
+// secret key from the seed: host int8 [N] (if sk8_host) and, if s_ntt, NTT form + Shoup [2][L][N]
+hy_status client_secret(const hy_params* p, u64 seed, int8_t* sk8_dev, u64* s_res, u64* s_ntt, cudaStream_t st) {
+  gen_secret_kernel<<<64, 256, 0, st>>>(seed, (int)p->L, (int)p->logN, qarr(p), s_res, sk8_dev);
+  HY_LAUNCH_CHECK();
+  if (!s_ntt) return HY_OK;
+  HY_TRY(ntt_poly_fwd(p, s_res, s_ntt, 1, st));
+  return shoup_table(p, s_ntt, s_ntt + (size_t)p->L * p->N, 1, st);
+}
+
+// n encryptions (indices idx[o]) of plaintexts m [n][N] (device) under the secret of `seed`
+hy_status client_encrypt(const hy_params* p, u64 seed, const u64* s_ntt, const u64* m_dev, const uint32_t* idx_dev,
+                         size_t n, const u64* delta_l, u64* ct_out, u64* work, cudaStream_t st) {
+  const size_t L = p->L, N = p->N;
+  u64* A = work;                          // [n][L][N]
+  u64* An = A + n * L * N;                // [n][L][N]
+  int32_t* E = reinterpret_cast<int32_t*>(An + n * L * N);  // [n][N]
+  MaskArgs ma{seed, 2u, (int)L, (int)p->logN, n, idx_dev, 0u, qarr(p)};
+  gen_mask_kernel<<<148 * 8, 256, 0, st>>>(ma, A);
+  HY_LAUNCH_CHECK();
+  gen_error_kernel<<<148 * 8, 256, 0, st>>>(seed, 3u, (int)p->logN, n, idx_dev, 0, E);
+  HY_LAUNCH_CHECK();
+  HY_TRY(ntt_poly_fwd(p, A, An, n, st));
+  QArr dl;
+  for (size_t l = 0; l < L; l++) dl.q[l] = delta_l[l];
+  ClientInvJob j{An, s_ntt, A, E, m_dev, nullptr, ct_out, (int)L, (int)N, 0, qarr(p), dl};
+  return launch_inv(p, j, n * L, st);
+}
+
+// switching keys for n_elts Galois elements (device elts) under the secret of `seed`:
+// keys_out [n][L digits][2][L limbs][N] coefficient form
+hy_status client_keygen(const hy_params* p, u64 seed, const u64* s_ntt, const int8_t* sk8_dev, const uint32_t* elts_dev,
+                        size_t n_elts, u64* keys_out, u64* work, cudaStream_t st) {
+  const size_t L = p->L, N = p->N, n = n_elts * L;  // polys groups o = element * L + digit
+  u64* A = work;                          // [n][L][N]
+  u64* An = A + n * L * N;
+  u64* Sg = An + n * L * N;               // [n_elts][L][N]
+  int32_t* E = reinterpret_cast<int32_t*>(Sg + n_elts * L * N);  // [n][N]
+  MaskArgs ma{seed, 4u, (int)L, (int)p->logN, n, elts_dev, 1u, qarr(p)};
+  gen_mask_kernel<<<148 * 8, 256, 0, st>>>(ma, A);
+  HY_LAUNCH_CHECK();
+  gen_error_kernel<<<148 * 8, 256, 0, st>>>(seed, 5u, (int)p->logN, n, elts_dev, (int)L, E);
+  HY_LAUNCH_CHECK();
+  automorph_secret_kernel<<<148 * 4, 256, 0, st>>>(sk8_dev, elts_dev, (int)n_elts, (int)L, (int)p->logN, qarr(p), Sg);
+  HY_LAUNCH_CHECK();
+  HY_TRY(ntt_poly_fwd(p, A, An, n, st));
+  QArr dl{};
+  ClientInvJob j{An, s_ntt, A, E, nullptr, Sg, keys_out, (int)L, (int)N, (int)L, qarr(p), dl};
+  return launch_inv(p, j, n * L, st);
 }
 
 hy_status decrypt_phase(const hy_params* p, const u64* s_ntt, const u64* s_ntt_sh, const u64* ct, size_t n, u64* x_out,

@@ -319,3 +319,212 @@ inline size_t ntt_smem_bytes() {
   constexpr int B = NttCfg<LOGN>::B;
   return (size_t)(B + B / 16) * sizeof(u64);
 }
+
+// =======================================================================================
+// One-CTA-per-transform NTT for N = 4096 / 8192 (the ring degrees of every N <= 8192 config):
+// T = N / 32 threads x 32 coefficients per thread, three register groups of butterfly stages
+// (5 + 5 + LOGN - 10 stages) separated by two shared-memory exchanges, plus one exchange that
+// applies the slot-order permutation.  Compared with ntt_fwd_kernel: no recomputed first stage,
+// 2 (not 4) exchanges, twiddles (w, w') as one 16-byte load, uniform (broadcast) twiddles in the
+// first group, and an XOR swizzle instead of padding (every exchange pattern is bank-conflict
+// free for 64-bit words, checked exhaustively for both N).
+//   group A (stages 0..4):  thread tid holds coefficients j = tid + T r           (r < 32)
+//   group B (stages 5..9):  j = (tid / D) 32 D + tid % D + D r,  D = N / 1024
+//   group C (stages 10..):  j = D (tid + T q) + r',  q < 32 / D, r' < D (D-point sub-blocks)
+// Twiddles: psi2[l][m + i] = (psi^{bitrev(m + i)}, Shoup companion) for the butterflies of block i
+// of stage log2 m (inverse: ipsi2 with psi^{-1}).  Forward values stay in Harvey's [0, 4q); the
+// inverse keeps [0, 2q) and folds N^{-1} into its last stage.
+// =======================================================================================
+template <int LOGN>
+struct Ntt2Cfg {
+  static constexpr int LOGV = 5, V = 32;
+  static constexpr int LOGT = LOGN - LOGV, T = 1 << LOGT;
+  static constexpr int LOGD = LOGN - 2 * LOGV, D = 1 << LOGD;
+  static constexpr int QN = V / D;  // sub-blocks per thread in group C
+};
+
+template <int LOGN>
+__device__ __forceinline__ int ntt2_sw(int k) {
+  if constexpr (LOGN == 13) return k ^ ((k >> 4) & 7) ^ (((k >> 8) & 1) << 3);
+  else return k ^ ((k >> 4) & 3) ^ (((k >> 7) & 3) << 2);
+}
+
+struct Ntt2Tables {
+  const ulonglong2* tw;   // [L][N] (w, w') forward (psi) or inverse (psi^{-1})
+  const int32_t* kos;     // [N] bit-reversed butterfly position of slot j
+};
+
+__device__ __forceinline__ u64 csub2(u64 x, u64 m) { return x >= m ? x - m : x; }
+
+template <int LOGN, class Job>
+__global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
+    ntt2_fwd_kernel(Job job, Ntt2Tables tb, LimbConsts L) {
+  pdl_begin();
+  using C = Ntt2Cfg<LOGN>;
+  constexpr int N = 1 << LOGN, T = C::T, V = C::V, D = C::D;
+  extern __shared__ u64 sm[];
+  const int tid = threadIdx.x;
+  Job jb = job;
+  jb.bind(blockIdx.x);
+  const int l = jb.limb;
+  const u64 q = L.lc[l].q, q2 = L.lc[l].two_q;
+  const ulonglong2* __restrict__ W = tb.tw + ((size_t)l << LOGN);
+  u64 v[V];
+#pragma unroll
+  for (int r = 0; r < V; r++) v[r] = jb.load(tid + T * r);
+  auto bfly = [&](u64& x, u64& y, const ulonglong2 w) {  // Harvey CT: [0, 4q) -> [0, 4q)
+    const u64 X = csub2(x, q2);
+    const u64 Tt = shoup_mul(y, w.x, w.y, q);
+    x = X + Tt;
+    y = X - Tt + q2;
+  };
+  // ---- group A: stages 0..4, twiddles uniform over the CTA ----
+#pragma unroll
+  for (int s = 0; s < 5; s++) {
+    const int h = 16 >> s;
+#pragma unroll
+    for (int r = 0; r < V; r++)
+      if ((r & h) == 0) bfly(v[r], v[r + h], __ldg(W + (1 << s) + (r >> (5 - s))));
+  }
+#pragma unroll
+  for (int r = 0; r < V; r++) sm[ntt2_sw<LOGN>(tid + T * r)] = v[r];
+  __syncthreads();
+  // ---- group B: stages 5..9 ----
+  const int blk = tid / D, baseB = blk * (D * V) + tid % D;
+#pragma unroll
+  for (int r = 0; r < V; r++) v[r] = sm[ntt2_sw<LOGN>(baseB + D * r)];
+#pragma unroll
+  for (int s = 5; s < 10; s++) {
+    const int h = 16 >> (s - 5);
+    const int sh = LOGN - s;  // log2 of the block size of stage s
+#pragma unroll
+    for (int r = 0; r < V; r++)
+      if ((r & h) == 0) bfly(v[r], v[r + h], __ldg(W + (1 << s) + (blk << (s - 5)) + ((D * r) >> sh)));
+  }
+  // (every thread rewrites exactly the positions it read: no barrier before the write-back)
+#pragma unroll
+  for (int r = 0; r < V; r++) sm[ntt2_sw<LOGN>(baseB + D * r)] = v[r];
+  __syncthreads();
+  // ---- group C: stages 10..LOGN-1 inside D-point sub-blocks ----
+#pragma unroll
+  for (int qq = 0; qq < C::QN; qq++)
+#pragma unroll
+    for (int rr = 0; rr < D; rr++) v[qq * D + rr] = sm[ntt2_sw<LOGN>(D * (tid + T * qq) + rr)];
+#pragma unroll
+  for (int s = 10; s < LOGN; s++) {
+    const int h = D >> (s - 9);
+#pragma unroll
+    for (int qq = 0; qq < C::QN; qq++)
+#pragma unroll
+      for (int rr = 0; rr < D; rr++)
+        if ((rr & h) == 0)
+          bfly(v[qq * D + rr], v[qq * D + rr + h],
+               __ldg(W + (1 << s) + ((tid + T * qq) << (s - 10)) + (rr >> (LOGN - s))));
+  }
+#pragma unroll
+  for (int qq = 0; qq < C::QN; qq++)
+#pragma unroll
+    for (int rr = 0; rr < D; rr++) {
+      const u64 x = csub2(csub2(v[qq * D + rr], q2), q);
+      sm[ntt2_sw<LOGN>(D * (tid + T * qq) + rr)] = x;
+    }
+  __syncthreads();
+  // ---- slot-order output: position j holds butterfly position kos[j] (coalesced stores) ----
+#pragma unroll 8
+  for (int r = 0; r < V; r++) {
+    const int j = tid + T * r;
+    jb.store(j, sm[ntt2_sw<LOGN>(__ldg(tb.kos + j))]);
+  }
+}
+
+template <int LOGN, class Job>
+__global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
+    ntt2_inv_kernel(Job job, Ntt2Tables tb, LimbConsts L) {
+  pdl_begin();
+  using C = Ntt2Cfg<LOGN>;
+  constexpr int N = 1 << LOGN, T = C::T, V = C::V, D = C::D;
+  extern __shared__ u64 sm[];
+  const int tid = threadIdx.x;
+  Job jb = job;
+  jb.bind(blockIdx.x);
+  const int l = jb.limb;
+  const u64 q = L.lc[l].q, q2 = L.lc[l].two_q;
+  const ulonglong2* __restrict__ W = tb.tw + ((size_t)l << LOGN);
+  // ---- slot-order input -> butterfly positions ----
+#pragma unroll 8
+  for (int r = 0; r < V; r++) {
+    const int j = tid + T * r;
+    sm[ntt2_sw<LOGN>(__ldg(tb.kos + j))] = jb.load(j);
+  }
+  __syncthreads();
+  u64 v[V];
+  auto bfly = [&](u64& x, u64& y, const ulonglong2 w) {  // Harvey GS: [0, 2q) -> [0, 2q)
+    const u64 U = csub2(x + y, q2);
+    const u64 Vv = x - y + q2;
+    y = shoup_mul(Vv, w.x, w.y, q);
+    x = U;
+  };
+  // ---- group C (stages LOGN-1 .. 10) ----
+#pragma unroll
+  for (int qq = 0; qq < C::QN; qq++)
+#pragma unroll
+    for (int rr = 0; rr < D; rr++) v[qq * D + rr] = sm[ntt2_sw<LOGN>(D * (tid + T * qq) + rr)];
+#pragma unroll
+  for (int s = LOGN - 1; s >= 10; s--) {
+    const int h = D >> (s - 9);
+#pragma unroll
+    for (int qq = 0; qq < C::QN; qq++)
+#pragma unroll
+      for (int rr = 0; rr < D; rr++)
+        if ((rr & h) == 0)
+          bfly(v[qq * D + rr], v[qq * D + rr + h],
+               __ldg(W + (1 << s) + ((tid + T * qq) << (s - 10)) + (rr >> (LOGN - s))));
+  }
+#pragma unroll
+  for (int qq = 0; qq < C::QN; qq++)
+#pragma unroll
+    for (int rr = 0; rr < D; rr++) sm[ntt2_sw<LOGN>(D * (tid + T * qq) + rr)] = v[qq * D + rr];
+  __syncthreads();
+  // ---- group B (stages 9 .. 5) ----
+  const int blk = tid / D, baseB = blk * (D * V) + tid % D;
+#pragma unroll
+  for (int r = 0; r < V; r++) v[r] = sm[ntt2_sw<LOGN>(baseB + D * r)];
+#pragma unroll
+  for (int s = 9; s >= 5; s--) {
+    const int h = 16 >> (s - 5);
+    const int sh = LOGN - s;
+#pragma unroll
+    for (int r = 0; r < V; r++)
+      if ((r & h) == 0) bfly(v[r], v[r + h], __ldg(W + (1 << s) + (blk << (s - 5)) + ((D * r) >> sh)));
+  }
+#pragma unroll
+  for (int r = 0; r < V; r++) sm[ntt2_sw<LOGN>(baseB + D * r)] = v[r];
+  __syncthreads();
+  // ---- group A (stages 4 .. 0), N^{-1} folded into stage 0 ----
+#pragma unroll
+  for (int r = 0; r < V; r++) v[r] = sm[ntt2_sw<LOGN>(tid + T * r)];
+#pragma unroll
+  for (int s = 4; s >= 1; s--) {
+    const int h = 16 >> s;
+#pragma unroll
+    for (int r = 0; r < V; r++)
+      if ((r & h) == 0) bfly(v[r], v[r + h], __ldg(W + (1 << s) + (r >> (5 - s))));
+  }
+  {
+    const u64 ni = L.lc[l].ninv, nis = L.lc[l].ninv_sh;
+    const ulonglong2 wn = __ldg(W);  // slot 0 of the inverse table: psi^{-1}-twiddle of stage 0 times N^{-1}
+#pragma unroll
+    for (int r = 0; r < 16; r++) {
+      const u64 x = v[r], y = v[r + 16];
+      const u64 a0 = csub2(shoup_mul(x + y, ni, nis, q), q);
+      const u64 a1 = csub2(shoup_mul(x - y + q2, wn.x, wn.y, q), q);
+      jb.store(tid + T * r, a0);
+      jb.store(tid + T * (r + 16), a1);
+    }
+  }
+}
+
+template <int LOGN>
+inline size_t ntt2_smem_bytes() {
+  return (size_t)(1 << LOGN) * sizeof(u64);
+}

@@ -16,8 +16,8 @@ __all__ = ["HyenaError", "hy_conv_shape", "hy_layout", "load_library", "library_
            "hy_plan_layout", "hy_params_create", "hy_params_destroy", "hy_keys_upload", "hy_encode_weights",
            "hy_weights_layout", "hy_weights_destroy", "hy_conv_eval", "hy_conv_eval_host", "hy_poly_mul",
            "hy_ntt_roundtrip", "hy_rotate", "hy_decrypt_debug", "hy_kernel_launches", "hy_weights_set_stage_events",
-           "hy_weights_mac_time", "hy_weights_mac_path", "hy_weights_set_mac_path", "MAC_PATHS", "layout_dict",
-           "EXPORTED"]
+           "hy_weights_mac_time", "hy_weights_mac_path", "hy_weights_set_mac_path", "hy_secret_key", "hy_keygen",
+           "hy_encrypt", "MAC_PATHS", "layout_dict", "EXPORTED"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 HY_MAX_TAPS = 49
@@ -27,7 +27,8 @@ HY_MAX_GALOIS = 64
 EXPORTED = ["hy_last_error", "hy_plan_layout", "hy_params_create", "hy_params_destroy", "hy_keys_upload",
             "hy_encode_weights", "hy_weights_layout", "hy_weights_destroy", "hy_conv_eval", "hy_conv_eval_host",
             "hy_poly_mul", "hy_ntt_roundtrip", "hy_rotate", "hy_decrypt_debug", "hy_kernel_launches",
-            "hy_weights_set_stage_events", "hy_weights_mac_time", "hy_weights_mac_path", "hy_weights_set_mac_path"]
+            "hy_weights_set_stage_events", "hy_weights_mac_time", "hy_weights_mac_path", "hy_weights_set_mac_path",
+            "hy_secret_key", "hy_keygen", "hy_encrypt"]
 
 # S2 + S3 kernel choices (include/hyena.h hy_weights_mac_path)
 MAC_PATHS = {"thin": 0, "tc_fused": 1, "tc_split": 2, "fp64_fused": 3, "fp64_split": 4, "tc_coef": 5}
@@ -96,6 +97,9 @@ def load_library() -> ctypes.CDLL:
         "hy_weights_mac_time": (i32, [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(u32)]),
         "hy_weights_mac_path": (i32, [vp, ctypes.POINTER(i32)]),
         "hy_weights_set_mac_path": (i32, [vp, i32]),
+        "hy_secret_key": (i32, [vp, u64, vp]),
+        "hy_keygen": (i32, [vp, u64, u32, vp, vp, ctypes.c_int]),
+        "hy_encrypt": (i32, [vp, u64, vp, sz, u32, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -270,3 +274,25 @@ def hy_weights_mac_path(w: int) -> str:
 
 def hy_weights_set_mac_path(w: int, path: str) -> None:
     _check(load_library().hy_weights_set_mac_path(w, MAC_PATHS[path]), "hy_weights_set_mac_path")
+
+
+def hy_secret_key(p: int, seed: int, N: int) -> np.ndarray:
+    """The ternary secret of `seed` (Philox counter stream, synth/philox.py) as int8 [N]."""
+    out = np.empty(N, dtype=np.int8)
+    _check(load_library().hy_secret_key(p, seed, out.ctypes.data), "hy_secret_key")
+    return out
+
+
+def hy_keygen(p: int, seed: int, galois_elts: Sequence[int], keys_out=None, upload: bool = True):
+    """Switching keys on the GPU; keys_out: CUDA uint64 tensor [n][L][2][L][N] or None."""
+    g = (ctypes.c_uint32 * max(1, len(galois_elts)))(*[int(x) for x in galois_elts])
+    ptr = _dev_ptr(keys_out) if keys_out is not None else None
+    _check(load_library().hy_keygen(p, seed, len(galois_elts), g, ptr, int(upload)), "hy_keygen")
+
+
+def hy_encrypt(p: int, seed: int, m: np.ndarray, ct_out, first: int = 0, stream=None):
+    """Encrypt the plaintext polynomials m (host uint64 [n][N], coefficients < t) into ct_out
+    (CUDA uint64 [n][2][L][N]) with encryption counters first .. first + n - 1."""
+    mm = np.ascontiguousarray(m, dtype=np.uint64)
+    _check(load_library().hy_encrypt(p, seed, mm.ctypes.data, mm.shape[0], first, _dev_ptr(ct_out),
+                                     _stream(stream)), "hy_encrypt")

@@ -82,7 +82,7 @@ def run(hy, W, shape, ct, keys, path):
             d_out = torch.full((lay.Jout, 2, len(PRIMES), N), 9, dtype=torch.uint64, device="cuda")
             hy.hy_conv_eval(w, d_in, d_out)
             torch.cuda.synchronize()
-            return d_out[OUTS].cpu().numpy(), lay
+            return d_out[OUTS[0]:OUTS[-1] + 1].cpu().numpy(), lay
         finally:
             hy.hy_weights_destroy(w)
     finally:

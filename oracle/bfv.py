@@ -31,6 +31,7 @@ class BFVParams:
     N: int
     primes: List[int]
     t: int
+    w: int = 0   # decomposition base 2^w INSIDE each RNS limb (0: one digit per limb, reading R5)
 
     def __post_init__(self):
         assert self.N & (self.N - 1) == 0
@@ -45,6 +46,16 @@ class BFVParams:
     @property
     def L(self) -> int:
         return len(self.primes)
+
+    @property
+    def V(self) -> int:
+        """Sub-digits per limb: ceil(max bit length / w) (1 without a sub-digit base)."""
+        return 1 if not self.w else -(-max(q.bit_length() for q in self.primes) // self.w)
+
+    @property
+    def ND(self) -> int:
+        """Gadget digits: limb i, sub-digit v -> digit i V + v."""
+        return self.L * self.V
 
 
 def crt(residues: Sequence[np.ndarray], primes: Sequence[int]) -> list:
@@ -120,28 +131,36 @@ def noise_budget_bits(P: BFVParams) -> float:
 
 
 def galois_keygen(P: BFVParams, s, g: int, a, e) -> np.ndarray:
-    """Switching key for X -> X^g under the RNS-digit gadget (reading R5):
-    digit i, limb l:  b_{i,l} = [-a_{i,l} s + e_i + [i == l] s(X^g)]_{q_l},  a_{i,l} uniform.
-    [i == l] is the residue mod q_l of the gadget g_i = (Q/q_i)[(Q/q_i)^{-1}]_{q_i}.
-    a: uint64 [L][L][N], e: [L][N].  Returns uint64 [L][2][L][N] (b first, then a)."""
-    L, N = P.L, P.N
+    """Switching key for X -> X^g under the RNS-digit gadget (reading R5), optionally refined by a
+    base-2^w decomposition inside each limb (PAPER.md:1470 [app] decomposition base; SURVEY §8(f)
+    NEXT-4): digit (i, v) has gadget g_{i,v} = (Q/q_i)[(Q/q_i)^{-1}]_{q_i} 2^{w v}, whose residue mod
+    q_l is [i == l] 2^{w v}:
+        b_{(i,v),l} = [-a_{(i,v),l} s + e_{(i,v)} + [i == l] 2^{w v} s(X^g)]_{q_l},  a uniform.
+    a: uint64 [ND][L][N], e: [ND][N].  Returns uint64 [ND][2][L][N] (b first, then a)."""
+    L, N, V = P.L, P.N, P.V
     s_g = ring.automorphism(np.asarray(s, dtype=np.int64), g)
-    key = np.empty((L, 2, L, N), dtype=np.uint64)
-    for i in range(L):
+    key = np.empty((P.ND, 2, L, N), dtype=np.uint64)
+    for dd in range(P.ND):
+        i, v = divmod(dd, V)
         for l, q in enumerate(P.primes):
-            a_s = _mul_sparse_first(s, a[i, l], q)
-            b = -(a_s.astype(object)) + np.asarray(e[i], dtype=np.int64).astype(object)
+            a_s = _mul_sparse_first(s, a[dd, l], q)
+            b = -(a_s.astype(object)) + np.asarray(e[dd], dtype=np.int64).astype(object)
             if i == l:
-                b = b + s_g.astype(object)
-            key[i, 0, l] = ring.canon(b % q, q)
-            key[i, 1, l] = a[i, l]
+                b = b + s_g.astype(object) * ((1 << (P.w * v)) % q)
+            key[dd, 0, l] = ring.canon(b % q, q)
+            key[dd, 1, l] = a[dd, l]
     return key
 
 
 def decompose(P: BFVParams, ct) -> List[np.ndarray]:
     """Hoisting step 1 ('PermDecomp', PAPER.md:375-377, :1472): digits d_i = [c1]_{q_i}
-    as integer polynomials with coefficients in [0, q_i)."""
-    return [ct[1, i].astype(np.int64) for i in range(P.L)]
+    as integer polynomials with coefficients in [0, q_i); with a sub-digit base 2^w each is
+    split further into its base-2^w digits d_{i,v} = floor(d_i / 2^{w v}) mod 2^w, v < V, so that
+    sum_v d_{i,v} 2^{w v} = d_i (digit order i V + v)."""
+    if not P.w:
+        return [ct[1, i].astype(np.int64) for i in range(P.L)]
+    mask = np.uint64((1 << P.w) - 1)
+    return [((ct[1, i] >> np.uint64(P.w * v)) & mask).astype(np.int64) for i in range(P.L) for v in range(P.V)]
 
 
 def rotate_hoisted(P: BFVParams, ct, digits, g: int, key) -> np.ndarray:
@@ -154,7 +173,7 @@ def rotate_hoisted(P: BFVParams, ct, digits, g: int, key) -> np.ndarray:
     for l, q in enumerate(P.primes):
         c0 = ring.automorphism_mod(ct[0, l], g, q).astype(object)
         c1 = np.zeros(N, dtype=object)
-        for i in range(L):
+        for i in range(len(digits)):   # L digits, or L V sub-digits (the key has as many rows)
             di = ring.canon(dg[i], q)
             c0 = c0 + ring.nc_mul(di, key[i, 0, l], q).astype(object)
             c1 = c1 + ring.nc_mul(di, key[i, 1, l], q).astype(object)

@@ -82,6 +82,9 @@ def plan(N: int, batch: int, Ci: int, Co: int, H: int, W: int, kh: int, kw: int,
     Hp = next_pow2(H + 2 * pad)
     if Hp * Wp <= row:
         mode, per_row = "blocks", row // (Hp * Wp)
+        if force_cn == 4:   # c_n = 4: a channel's group is a quarter of the slots (half a slot row)
+            per_row = (row // 2) // (Hp * Wp)
+            assert per_row >= 1, "c_n = 4 needs an image block within N/4 slots"
         Hb = Hv = 0
         bands = 1
         G = -(-batch // per_row)
@@ -97,10 +100,15 @@ def plan(N: int, batch: int, Ci: int, Co: int, H: int, W: int, kh: int, kw: int,
         cn = force_cn
     else:
         cn = 2 if G <= 1 else 1
-    assert cn in (1, 2)
+    assert cn in (1, 2, 4)
     if depthwise:
         assert Ci == Co
-    if cn == 2:
+    if cn == 4:   # NEXT-1: Walsh-Hadamard packing of 4 channels, one unit
+        assert mode == "blocks" and G == 1 and not depthwise
+        U = 1
+        Jc = -(-Ci // 4)
+        Jo = -(-Co // 4)
+    elif cn == 2:
         U = G
         Jc = -(-Ci // 2)
         Jo = Jc if depthwise else -(-Co // 2)
@@ -153,8 +161,12 @@ def _group_out_slots(p: Plan, gamma: int):
 
 
 def _ct_rows_in(p: Plan, ct_index: int):
-    """(channel, group) held by slot rows 0 and 1 of input ciphertext ct_index (None = empty)."""
+    """(channel, group) held by the slot groups of input ciphertext ct_index (None = empty): slot
+    rows 0 and 1 (c_n <= 2), or for c_n = 4 the four groups c = 2 h + r (slot row r, half h of
+    the row) holding channels 4j + c."""
     u, j = divmod(ct_index, p.Jc)
+    if p.cn == 4:
+        return [(4 * j + c, u) if 4 * j + c < p.Ci else None for c in range(4)]
     if p.cn == 2:
         return [(2 * j + r, u) if 2 * j + r < p.Ci else None for r in range(2)]
     return [(j, 2 * u + r) if 2 * u + r < p.G else None for r in range(2)]
@@ -163,28 +175,37 @@ def _ct_rows_in(p: Plan, ct_index: int):
 def _ct_rows_out(p: Plan, ct_index: int):
     C = p.Ci if p.depthwise else p.Co
     u, j = divmod(ct_index, p.Jo)
+    if p.cn == 4:
+        return [(4 * j + c, u) if 4 * j + c < C else None for c in range(4)]
     if p.cn == 2:
         return [(2 * j + r, u) if 2 * j + r < C else None for r in range(2)]
     return [(j, 2 * u + r) if 2 * u + r < p.G else None for r in range(2)]
 
 
+def _group_base(p: Plan, c: int) -> int:
+    """First slot of slot group c (row-major slot vector: row 0 slots, then row 1 slots)."""
+    half = p.N // 2
+    if p.cn == 4:
+        return (c & 1) * half + (c >> 1) * (half // 2)
+    return c * half
+
+
 def pack(p: Plan, x: np.ndarray, t: int) -> np.ndarray:
     """x[batch][Ci][H][W] -> slot vectors [J][N] mod t (row 0 slots, then row 1 slots)."""
-    half = p.N // 2
     out = np.zeros((p.J, p.N), dtype=np.int64)
     for ci in range(p.J):
         for r, cg in enumerate(_ct_rows_in(p, ci)):
             if cg is None:
                 continue
             c, gamma = cg
+            base = _group_base(p, r)
             for b, y, xx, s in _group_slots(p, gamma):
-                out[ci, r * half + s] = int(x[b, c, y, xx]) % t
+                out[ci, base + s] = int(x[b, c, y, xx]) % t
     return out
 
 
 def unpack(p: Plan, slots: np.ndarray) -> np.ndarray:
     """slot vectors [Jout][N] -> y[batch][Co][Hout][Wout] (raw residues mod t)."""
-    half = p.N // 2
     C = p.Ci if p.depthwise else p.Co
     y = np.zeros((p.batch, C, p.Hout, p.Wout), dtype=np.int64)
     for ci in range(p.Jout):
@@ -192,8 +213,9 @@ def unpack(p: Plan, slots: np.ndarray) -> np.ndarray:
             if cg is None:
                 continue
             c, gamma = cg
+            base = _group_base(p, r)
             for b, yy, xx, s in _group_out_slots(p, gamma):
-                y[b, c, yy, xx] = slots[ci, r * half + s]
+                y[b, c, yy, xx] = slots[ci, base + s]
     return y
 
 
@@ -232,13 +254,39 @@ class LayerSetup:
     galois: List[int]   # required Galois elements (taps with step != 0, then row swap)
 
 
+def hadamard(n: int) -> np.ndarray:
+    """Sylvester's Walsh-Hadamard matrix H_n (reading R11): H_1 = [1], H_2m = [[H, H], [H, -H]]."""
+    H = np.array([[1]], dtype=np.int64)
+    while H.shape[0] < n:
+        H = np.block([[H, H], [H, -H]])
+    return H
+
+
+def align_elts(N: int) -> List[int]:
+    """c_n = 4 alignment: diagonal d = 2 dh + dr moves slot group c to c xor d by the row swap
+    (dr; X -> X^{2N-1}) and the half-row rotation (dh; left rotation by N/4 = X -> X^{3^{N/4}}),
+    one automorphism g_d = (2N-1)^dr (3^{N/4})^dh mod 2N for d = 1, 2, 3."""
+    gs = []
+    for d in (1, 2, 3):
+        g = 1
+        if d & 1:
+            g = g * rowswap_elt(N) % (2 * N)
+        if d & 2:
+            g = g * galois_elt_for_step(N, N // 4) % (2 * N)
+        gs.append(g)
+    return gs
+
+
 def setup(p: Plan, t: int, k: int = 0) -> LayerSetup:
-    """S0: h_{t,N} by encoding, k by find_k, sign-plaintext coefficient."""
+    """S0: h_{t,N} by encoding, k by find_k, sign-plaintext coefficient.
+    c_n = 4: no k (the dense Hadamard rows have no small multiple), output scale 4."""
     h = h_pn(t, p.N) if p.cn == 2 else 0
     if p.cn == 2:
         k = k or find_k(t, h)
         sc = centered(k * h, t)
         scale = 2 * k
+    elif p.cn == 4:
+        k, sc, scale = 1, 0, 4
     else:
         k, sc, scale = 1, 0, 1
     gal = []
@@ -249,7 +297,28 @@ def setup(p: Plan, t: int, k: int = 0) -> LayerSetup:
                 gal.append(g)
     if p.cn == 2 and not p.depthwise:
         gal.append(rowswap_elt(p.N))
+    if p.cn == 4:
+        gal.extend(g for g in align_elts(p.N) if g not in gal)
     return LayerSetup(p, k, scale, sc, h, gal)
+
+
+def hadamard_row_polys(P: bfv.BFVParams, p: Plan) -> List[List[np.ndarray]]:
+    """c_n = 4: the plaintexts of Hadamard rows r = 1..3, slot group c filled with H_4[r][c]
+    (Sylvester basis), encoded (oracle/encoding.py) and centered-lifted into every
+    limb (reading R14).  Row 0 is the constant 1.  Returns [r - 1][limb] polynomials."""
+    from .encoding import encode
+    H = hadamard(4)
+    half = P.N // 2
+    out = []
+    for r in (1, 2, 3):
+        slots = np.zeros(P.N, dtype=np.int64)
+        for c in range(4):
+            b = _group_base(p, c)
+            slots[b:b + half // 2] = H[r][c] % P.t
+        m = encode(slots, P.t, P.N)
+        cen = [centered(int(x), P.t) for x in m]
+        out.append([np.array([x % q for x in cen], dtype=np.uint64) for q in P.primes])
+    return out
 
 
 def sign_poly(P: bfv.BFVParams, ls: LayerSetup) -> List[np.ndarray]:
@@ -335,8 +404,44 @@ def he_conv(P: bfv.BFVParams, ls: LayerSetup, Wt: np.ndarray, ct_in: np.ndarray,
     T = len(p.taps)
     res = {}
     S = sign_poly(P, ls) if p.cn == 2 else None
+    if p.cn == 4:
+        HR = hadamard_row_polys(P, p)
+        H4 = hadamard(4)
+        G4 = align_elts(P.N)
     for oc in out_cts:
         u, go = divmod(oc, p.Jo)
+        if p.cn == 4:
+            # ProposedConv of Algorithm 1 with c_n = 4 (PAPER.md:1530-1551 [ign], :565-572): per
+            # diagonal d (input group c pairs with output channel 4g + (c xor d)), Hadamard filter
+            # scalars s_r = sum_c H_4[r][c] w_c, lazy MAC of s_r R per Hadamard row r, ONE
+            # reduction, PMult by the row-r plaintext, HAdd over r; then diagonal d is aligned by
+            # HRot with g_d (group c -> c xor d) and added (PAPER.md:574-579 generalised).
+            Pd = []
+            for d in range(4):
+                terms = [[] for _ in range(4)]
+                for j in range(p.Jc):
+                    for tau in range(T):
+                        wc = [_weight(Wt, p, 4 * go + (c ^ d), 4 * j + c, tau) for c in range(4)]
+                        Rjt = R[(u * p.Jc + j, tau)]
+                        for r in range(4):
+                            terms[r].append((int(sum(H4[r][c] * wc[c] for c in range(4))), Rjt))
+                A = [_lincomb(P, terms[r]) for r in range(4)]
+                part = np.empty((2, P.L, P.N), dtype=np.uint64)
+                for comp in range(2):
+                    for l, q in enumerate(P.primes):
+                        acc = A[0][comp, l].astype(object)
+                        for r in (1, 2, 3):
+                            acc = acc + ring.nc_mul(HR[r - 1][l], A[r][comp, l], q).astype(object)
+                        part[comp, l] = (acc % q).astype(np.uint64)
+                Pd.append(part)
+            out = Pd[0].copy()
+            for d in (1, 2, 3):
+                sw = bfv.hrot(P, Pd[d], G4[d - 1], keys[G4[d - 1]])
+                for comp in range(2):
+                    for l, q in enumerate(P.primes):
+                        out[comp, l] = ring.add_mod(out[comp, l], sw[comp, l], q)
+            res[oc] = out
+            continue
         if p.cn == 1:
             # padded convolution: Out = sum_{c,tau} W[o][c][tau] R_{c,tau}
             terms = []

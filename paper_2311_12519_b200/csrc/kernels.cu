@@ -1834,9 +1834,9 @@ hy_status launch_ksmac_tc_t(const KsMacArgs& a, const int8_t* w8, int units, cud
 template <int LT>
 hy_status launch_ksmac_tc(const KsMacArgs& a, const int8_t* w8, int units, cudaStream_t s) {
   const bool uni = a.Jcb % 4 == 0 && a.K % 4 == 0 && !a.dbg;
-  // HY_KSMAC=1: the non-persistent Shoup-producer kernel, 2: the persistent Shoup-producer kernel,
-  // default (3): the persistent exact-product kernel (A/B measurements)
-  static const int ver = getenv("HY_KSMAC") ? atoi(getenv("HY_KSMAC")) : 3;
+  // default (2): the persistent Shoup-producer kernel; HY_KSMAC=1: the non-persistent one, 3: the
+  // persistent exact-product kernel (A/B measurements: measured slower at C4)
+  static const int ver = getenv("HY_KSMAC") ? atoi(getenv("HY_KSMAC")) : 2;
   if (uni && !a.coef && ver == 3 && a.Mpad <= 128 && a.wblocks == 1) {
     const V2Geom g = v3_geom(a.T, LT, a.Kpad, 232448);
     if (g.S >= 2) {

@@ -59,14 +59,14 @@ inline V2Geom v2_geom(int T, int L, int Kpad, size_t smem_max) {
     for (int S = 4; S >= 2; S--) {
       const uint32_t w = wres ? wbytes : 0;
       const uint32_t per = V2_STAGE_B + (wres ? 0 : V2_STAGE_A);
-      const size_t tot = 1024 + (size_t)w + (size_t)S * per + 2 * (size_t)g.key_bytes + bar;
+      const size_t tot = 1024 + (size_t)w + (size_t)S * per + 3 * (size_t)g.key_bytes + bar;
       if (tot <= smem_max) {
         g.S = S;
         g.wres = wres;
         g.off_b = w;
         g.off_a = w + S * V2_STAGE_B;
         g.off_key = g.off_a + (wres ? 0 : S * V2_STAGE_A);
-        g.off_bar = g.off_key + 2 * g.key_bytes;
+        g.off_bar = g.off_key + 3 * g.key_bytes;
         g.bytes = tot;
         return g;
       }
@@ -110,9 +110,9 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
   uint64_t* const empty_bar = bars + 4;       // [S]  UMMA completion -> producers
   uint64_t* const tfull = bars + 8;           // [2]  accumulator complete -> epilogue
   uint64_t* const tempty = bars + 10;         // [2]  accumulator read -> UMMA issuer
-  uint64_t* const kfull = bars + 12;          // [2]  key buffer landed (cp.async arrivals)
-  uint64_t* const kempty = bars + 14;         // [2]  key buffer no longer read
-  uint32_t* const s_tmem = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* const kfull = bars + 12;          // [3]  key buffer landed (cp.async arrivals)
+  uint64_t* const kempty = bars + 15;         // [3]  key buffer no longer read
+  uint32_t* const s_tmem = reinterpret_cast<uint32_t*>(bars + 18);
 
   constexpr bool CN = LOGN > 0;
   const int N = CN ? (1 << LOGN) : (1 << a.logN);
@@ -135,6 +135,8 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
     for (int b = 0; b < 2; b++) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], EPI);
+    }
+    for (int b = 0; b < 3; b++) {
       mbar_init(&kfull[b], V2_PROD);
       mbar_init(&kempty[b], V2_PROD_WARPS);
     }
@@ -157,13 +159,13 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
   const uint32_t tmem = *s_tmem;
 
   // key words of tile `it` of this CTA (limb l, positions j0 .. j0 + 15, every tap), copied by the
-  // producer threads into key buffer it & 1: [tap][x = 2i + comp][val, sh][16]; every producer
-  // thread arrives (cp.async.mbarrier.arrive.noinc) on kfull[it & 1] when its copies have landed
+  // producer threads into key buffer it % 3: [tap][x = 2i + comp][val, sh][16]; every producer
+  // thread arrives (cp.async.mbarrier.arrive.noinc) on kfull[it % 3] when its copies have landed
   auto issue_keys = [&](int it) {
     const int tile = blockIdx.x + it * gridDim.x;
     const int rem = tile % per_unit;
     const int l = rem / tiles_pl, j0 = (rem % tiles_pl) * TC_POS;
-    const uint32_t kb = sm_a + geo.off_key + (uint32_t)(it & 1) * geo.key_bytes;
+    const uint32_t kb = sm_a + geo.off_key + (uint32_t)(it % 3) * geo.key_bytes;
     const int pieces = a.T * 4 * LT * (TC_POS / 2);
     for (int e = threadIdx.x; e < pieces; e += V2_PROD) {
       const int p2 = e % (TC_POS / 2), r = e / (TC_POS / 2);
@@ -173,12 +175,13 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
         v2_cp16(kb + (uint32_t)e * 16,
                 key + (size_t)sh * 2 * LT * LN + (size_t)x * LN + (size_t)l * N + j0 + 2 * p2);
     }
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&kfull[it & 1])) : "memory");
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&kfull[it % 3])) : "memory");
   };
 
   if (warp < V2_PROD_WARPS) {
     // ======================= producers =======================
     if (my_tiles > 0) issue_keys(0);
+    if (my_tiles > 1) issue_keys(1);
     uint64_t ident = 0;  // taps without a key (the identity rotation)
     for (int t = 0; t < a.T; t++)
       if (a.tt.key[t] == nullptr) ident |= 1ull << t;
@@ -188,7 +191,6 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
     const int ks = tg >> 3, kg = tg & 7;
     const uint32_t off0 = (pos >> 3) * 256 + (kg >> 2) * 128 + (pos & 7) * 16 + (kg & 3) * 4;
     const uint32_t off1 = off0 + 2 * 256;
-    const int ch_issue = nchunks - 1;  // chunk of a tile at which the next tile's keys are issued (all warps long past the previous tile)
     struct Term {
       u64 c0, d[LT];
     };
@@ -244,13 +246,13 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
     int cit = 0, cch = 0, gc = 0;
     u64 q = 0;
     auto step = [&](Term* cur, int grp, Term* nxt, int& grp_nxt) {
-      if (cch == 0) {  // a new tile: its keys must have landed
+      if (cch == 0) {  // a new tile: its keys must have landed; prefetch those of tile cit + 2
         q = a.lcs.lc[((blockIdx.x + cit * gridDim.x) % per_unit) / tiles_pl].q;
-        mbar_wait(&kfull[cit & 1], (cit >> 1) & 1);
-      }
-      if (cch == ch_issue && cit + 1 < my_tiles) {  // prefetch the next tile's keys into the other buffer
-        if (cit >= 1) mbar_wait(&kempty[(cit + 1) & 1], ((cit - 1) >> 1) & 1);
-        issue_keys(cit + 1);
+        if (cit + 2 < my_tiles) {  // buffer (cit + 2) % 3 was last read by tile cit - 1
+          if (cit >= 1) mbar_wait(&kempty[(cit + 2) % 3], ((cit - 1) / 3) & 1);
+          issue_keys(cit + 2);
+        }
+        mbar_wait(&kfull[cit % 3], (cit / 3) & 1);
       }
       if (gc + 1 < my_tiles * nchunks) load(nxt, grp_nxt);
       uint32_t lo0[4], hi0[4], lo1[4], hi1[4];
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
           hi1[t] = (uint32_t)(cur[t].d[0] >> 32);
         }
       } else {
-        const uint32_t kp = sm_a + geo.off_key + (uint32_t)(cit & 1) * geo.key_bytes + (uint32_t)pos * 8 +
+        const uint32_t kp = sm_a + geo.off_key + (uint32_t)(cit % 3) * geo.key_bytes + (uint32_t)pos * 8 +
                             (uint32_t)grp * (4 * LT * TC_POS * 8);
         u64 r0[4], r1[4];
 #pragma unroll
@@ -297,7 +299,7 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
       }
       if (cch == nchunks - 1) {  // this warp is done reading the tile's keys
         __syncwarp();
-        if (lane == 0) mbar_arrive(&kempty[cit & 1]);
+        if (lane == 0) mbar_arrive(&kempty[cit % 3]);
       }
       uint32_t p0[8], p1[8];
       byte_tr4(lo0, p0);

@@ -37,14 +37,14 @@ inline V2Geom v3_geom(int T, int L, int Kpad, size_t smem_max) {
     for (int S = 3; S >= 2; S--) {
       const uint32_t w = wres ? wbytes : 0;
       const uint32_t per = V3_STAGE_B + (wres ? 0 : V3_STAGE_A);
-      const size_t tot = 1024 + (size_t)w + (size_t)S * per + 2 * (size_t)g.key_bytes + bar;
+      const size_t tot = 1024 + (size_t)w + (size_t)S * per + 3 * (size_t)g.key_bytes + bar;
       if (tot <= smem_max) {
         g.S = S;
         g.wres = wres;
         g.off_b = w;
         g.off_a = w + S * V3_STAGE_B;
         g.off_key = g.off_a + (wres ? 0 : S * V3_STAGE_A);
-        g.off_bar = g.off_key + 2 * g.key_bytes;
+        g.off_bar = g.off_key + 3 * g.key_bytes;
         g.bytes = tot;
         return g;
       }
@@ -106,6 +106,13 @@ __device__ __forceinline__ void tc_store4_g(const KsMacArgs& a, int z, int row, 
   reinterpret_cast<ulonglong2*>(a.out + at)[1] = make_ulonglong2(v[2], v[3]);
 }
 
+// 32 x 32 + 64 -> 64-bit multiply-add: one IMAD.WIDE.U32
+__device__ __forceinline__ u64 madw(uint32_t a, uint32_t b, u64 c) {
+  u64 d;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+  return d;
+}
+
 template <int LT, int LOGN, int EPI>
 __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
     ksmac_v3_kernel(KsMacArgs a, const int8_t* __restrict__ w8, V2Geom geo, int units) {
@@ -120,9 +127,9 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
   uint64_t* const empty_bar = bars + 4;       // [S]  UMMA completion -> producers
   uint64_t* const tfull = bars + 8;           // [2]  accumulator complete -> epilogue
   uint64_t* const tempty = bars + 10;         // [2]  accumulator read -> UMMA issuer
-  uint64_t* const kfull = bars + 12;          // [2]  key buffer landed (cp.async arrivals)
-  uint64_t* const kempty = bars + 14;         // [2]  key buffer no longer read
-  uint32_t* const s_tmem = reinterpret_cast<uint32_t*>(bars + 16);
+  uint64_t* const kfull = bars + 12;          // [3]  key buffer landed (cp.async arrivals)
+  uint64_t* const kempty = bars + 15;         // [3]  key buffer no longer read
+  uint32_t* const s_tmem = reinterpret_cast<uint32_t*>(bars + 18);
 
   constexpr bool CN = LOGN > 0;
   const int N = CN ? (1 << LOGN) : (1 << a.logN);
@@ -144,6 +151,8 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
     for (int b = 0; b < 2; b++) {
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], EPI);
+    }
+    for (int b = 0; b < 3; b++) {
       mbar_init(&kfull[b], V2_PROD);
       mbar_init(&kempty[b], V2_PROD_WARPS);
     }
@@ -166,12 +175,12 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
   const uint32_t tmem = *s_tmem;
 
   // split key words of tile `it` (limb l, positions j0 .. j0 + 7): [tap][digit i][b, a][8] from the
-  // key's third block; every producer thread arrives on kfull[it & 1] when its copies landed
+  // key's third block; every producer thread arrives on kfull[it % 3] when its copies landed
   auto issue_keys = [&](int it) {
     const int tile = blockIdx.x + it * gridDim.x;
     const int rem = tile % per_unit;
     const int l = rem / tiles_pl, j0 = (rem % tiles_pl) * V3_POS;
-    const uint32_t kb = sm_a + geo.off_key + (uint32_t)(it & 1) * geo.key_bytes;
+    const uint32_t kb = sm_a + geo.off_key + (uint32_t)(it % 3) * geo.key_bytes;
     const int pieces = a.T * LT * 2 * (V3_POS / 2);
     for (int e = threadIdx.x; e < pieces; e += V2_PROD) {
       const int p2 = e % (V3_POS / 2), r = e / (V3_POS / 2);  // r = (tap L + i) 2 + comp
@@ -181,12 +190,13 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
         v2_cp16(kb + (uint32_t)e * 16,
                 key + (size_t)4 * LT * LN + (size_t)(2 * i + comp) * LN + (size_t)l * N + j0 + 2 * p2);
     }
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&kfull[it & 1])) : "memory");
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&kfull[it % 3])) : "memory");
   };
 
   if (warp < V2_PROD_WARPS) {
     // ======================= producers =======================
     if (my_tiles > 0) issue_keys(0);
+    if (my_tiles > 1) issue_keys(1);
     uint64_t ident = 0;
     for (int t = 0; t < a.T; t++)
       if (a.tt.key[t] == nullptr) ident |= 1ull << t;
@@ -196,7 +206,6 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
     const int ks = tg >> 3, kg = tg & 7;
     // plane b, component c: K-major core-matrix group 2b + c, row pos, 4 bytes at term 4 kg
     const uint32_t offp = (kg >> 2) * 128 + pos * 16 + (kg & 3) * 4;
-    const int ch_issue = nchunks > 1 ? nchunks - 1 : 0;
     struct Term {
       u64 c0, d[LT];
     };
@@ -249,10 +258,12 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
     };
     int cit = 0, cch = 0, gc = 0;
     auto step = [&](Term* cur, int grp, Term* nxt, int& grp_nxt) {
-      if (cch == 0) mbar_wait(&kfull[cit & 1], (cit >> 1) & 1);
-      if (cch == ch_issue && cit + 1 < my_tiles) {
-        if (cit >= 1) mbar_wait(&kempty[(cit + 1) & 1], ((cit - 1) >> 1) & 1);
-        issue_keys(cit + 1);
+      if (cch == 0) {  // a new tile: prefetch the keys of tile cit + 2, wait for its own
+        if (cit + 2 < my_tiles) {  // buffer (cit + 2) % 3 was last read by tile cit - 1
+          if (cit >= 1) mbar_wait(&kempty[(cit + 2) % 3], ((cit - 1) / 3) & 1);
+          issue_keys(cit + 2);
+        }
+        mbar_wait(&kfull[cit % 3], (cit / 3) & 1);
       }
       if (gc + 1 < my_tiles * nchunks) load(nxt, grp_nxt);
       // w[t][k]: 32-bit words of term t: k = 0..3 -> R.c0 bits 0-31, 32-63, 64-95, 96-127; 4..7 -> R.c1
@@ -273,7 +284,7 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
           w[t][6] = w[t][7] = 0;
         }
       } else {
-        const uint32_t kp = sm_a + geo.off_key + (uint32_t)(cit & 1) * geo.key_bytes + (uint32_t)pos * 8 +
+        const uint32_t kp = sm_a + geo.off_key + (uint32_t)(cit % 3) * geo.key_bytes + (uint32_t)pos * 8 +
                             (uint32_t)grp * (LT * 2 * V3_POS * 8);
         uint32_t kb0[LT], kb1[LT], ka0[LT], ka1[LT];
 #pragma unroll
@@ -292,14 +303,14 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
 #pragma unroll
           for (int i = 0; i < LT; i++) {
             const uint32_t d0 = (uint32_t)cur[t].d[i] & 0x3FFFFFFFu, d1 = (uint32_t)(cur[t].d[i] >> 30);
-            p0 += (u64)d0 * kb0[i];
-            p1 += (u64)d0 * kb1[i];
-            p1 += (u64)d1 * kb0[i];
-            p2 += (u64)d1 * kb1[i];
-            r0 += (u64)d0 * ka0[i];
-            r1 += (u64)d0 * ka1[i];
-            r1 += (u64)d1 * ka0[i];
-            r2 += (u64)d1 * ka1[i];
+            p0 = madw(d0, kb0[i], p0);
+            p1 = madw(d0, kb1[i], p1);
+            p1 = madw(d1, kb0[i], p1);
+            p2 = madw(d1, kb1[i], p2);
+            r0 = madw(d0, ka0[i], r0);
+            r1 = madw(d0, ka1[i], r1);
+            r1 = madw(d1, ka0[i], r1);
+            r2 = madw(d1, ka1[i], r2);
           }
           // R = P0 + P1 2^30 + P2 2^60 exactly (< 2^124), as 128 bits
           const u128 R0 = (u128)p0 + ((u128)p1 << 30) + ((u128)p2 << 60);
@@ -316,7 +327,7 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
       }
       if (cch == nchunks - 1) {  // this warp is done reading the tile's keys
         __syncwarp();
-        if (lane == 0) mbar_arrive(&kempty[cit & 1]);
+        if (lane == 0) mbar_arrive(&kempty[cit % 3]);
       }
       // byte transposes: plane 4k + b of component c gets byte b of word 4c + k of the 4 terms
       uint32_t pl[8][4];

@@ -31,8 +31,8 @@ class Layer:
 def keygen(P: bfv.BFVParams, s, elts: List[int], seed: int) -> Dict[int, np.ndarray]:
     keys = {}
     for n, g in enumerate(elts):
-        a = synth.uniform_residues(synth.rng(seed, "a", 100000 + n), P.primes, (P.L, P.N))
-        e = synth.cbd(synth.rng(seed, "e", 100000 + n), (P.L, P.N))
+        a = synth.uniform_residues(synth.rng(seed, "a", 100000 + n), P.primes, (P.ND, P.N))
+        e = synth.cbd(synth.rng(seed, "e", 100000 + n), (P.ND, P.N))
         keys[g] = bfv.galois_keygen(P, s, g, a, e)
     return keys
 
@@ -51,8 +51,8 @@ def encrypt_slots(P: bfv.BFVParams, s, slots: np.ndarray, seed: int) -> np.ndarr
 
 def make_layer(N: int, primes: List[int], batch: int, Ci: int, Co: int, H: int, W: int, kh: int, kw: int,
                pad: int, depthwise: bool = False, xrange=(-8, 8), wrange=(-8, 8), seed: int = 50,
-               force_cn: int = 0, k: int = 0, t: int = synth.T_PLAIN, x=None, Wt=None) -> Layer:
-    P = bfv.BFVParams(N, list(primes), t)
+               force_cn: int = 0, k: int = 0, t: int = synth.T_PLAIN, x=None, Wt=None, w: int = 0) -> Layer:
+    P = bfv.BFVParams(N, list(primes), t, w=w)
     p = conv.plan(N, batch, Ci, Co, H, W, kh, kw, pad, depthwise, force_cn)
     ls = conv.setup(p, t, k)
     if x is None:

@@ -28,8 +28,8 @@ def _enc(P, s, slots, stream):
 
 
 def _key(P, s, g, stream):
-    a = synth.uniform_residues(synth.rng(92, "a", stream), P.primes, (P.L, P.N))
-    e = synth.cbd(synth.rng(92, "e", stream), (P.L, P.N))
+    a = synth.uniform_residues(synth.rng(92, "a", stream), P.primes, (P.ND, P.N))
+    e = synth.cbd(synth.rng(92, "e", stream), (P.ND, P.N))
     return bfv.galois_keygen(P, s, g, a, e)
 
 
@@ -126,3 +126,56 @@ def test_decrypt_rounding_is_exact_at_boundary():
         for l, q in enumerate(P.primes):
             ct[0, l, 0] = x % q
         assert (bfv.decrypt(P, ct, s)[0] == m0) == ok
+
+
+# ---------------------------------------------------------------------------------------------
+# sub-digit decomposition base (PAPER.md:1470 [app] "decomposition base")
+# ---------------------------------------------------------------------------------------------
+def test_subdigit_gadget_reconstructs_c1():
+    """The gadget identity, written out: for every limb l, sum_{i,v} d_{i,v} g_{i,v} = c1 (mod q_l)
+    with g_{i,v} = [i == l] 2^{w v} mod q_l, and every digit below 2^w."""
+    for w in (13, 20, 25, 50):
+        P = bfv.BFVParams(64, ntt_primes(64, 50, 3), T, w=w)
+        assert P.V == -(-50 // w) and P.ND == 3 * P.V
+        c1 = synth.uniform_residues(synth.rng(93, "ct", w), P.primes, (P.N,))
+        ct = np.stack([c1, c1])
+        d = bfv.decompose(P, ct)
+        assert len(d) == P.ND and all(int(x.max()) < (1 << w) and int(x.min()) >= 0 for x in d)
+        for l, q in enumerate(P.primes):
+            acc = np.zeros(P.N, dtype=object)
+            for dd, x in enumerate(d):
+                i, v = divmod(dd, P.V)
+                if i == l:
+                    acc = acc + x.astype(object) * pow(2, w * v)
+            assert list(acc % q) == [int(y) for y in c1[l]]
+
+
+def test_subdigit_key_relation_and_rotation():
+    """b + a s = e + [i == l] 2^{w v} s(X^g) (mod q_l) for every digit row; the hoisted rotation
+    with the sub-digit key decrypts to the rotated slots; its key-switching noise is far below
+    the one-digit-per-limb gadget's (the reason for a smaller base: PAPER.md:587-617)."""
+    N = 256
+    P1 = bfv.BFVParams(N, ntt_primes(N, 50, 2), T)
+    P2 = bfv.BFVParams(N, ntt_primes(N, 50, 2), T, w=20)
+    s = synth.ternary(synth.rng(94, "sk"), N)
+    g = galois_elt_for_step(N, 3)
+    key = _key(P2, s, g, 7)
+    assert key.shape == (P2.ND, 2, 2, N)
+    sg = ring.automorphism(np.asarray(s), g)
+    e = synth.cbd(synth.rng(92, "e", 7), (P2.ND, N))
+    for dd in range(P2.ND):
+        i, v = divmod(dd, P2.V)
+        for l, q in enumerate(P2.primes):
+            lhs = (key[dd, 0, l].astype(object) + ring.nc_mul(np.asarray(s), key[dd, 1, l], q).astype(object)) % q
+            rhs = (np.asarray(e[dd]).astype(object) + (sg.astype(object) * pow(2, 20 * v) if i == l else 0)) % q
+            assert list(lhs) == list(rhs)
+    v = np.arange(N) * 31 % T
+    noise = []
+    for P in (P1, P2):
+        ct, m = _enc(P, s, v, 3)
+        rot = bfv.hrot(P, ct, g, _key(P, s, g, 7))
+        exp = np.concatenate([np.roll(v[:N // 2], -3), np.roll(v[N // 2:], -3)])
+        dec = bfv.decrypt(P, rot, s)
+        assert list(decode(dec, T, N)) == list(exp)
+        noise.append(bfv.noise_bits(P, rot, s, dec))
+    assert noise[1] < noise[0] - 20, noise

@@ -138,3 +138,71 @@ def test_c1_config_end_to_end():
     for i, ct in out.items():
         dec = bfv.decrypt(lay.P, ct, lay.s)
         assert budget - bfv.noise_bits(lay.P, ct, lay.s, dec) >= 4
+
+
+# ---------------------------------------------------------------------------------------------
+# c_n = 4 Walsh-Hadamard channel packing (reading R11)
+# ---------------------------------------------------------------------------------------------
+def test_sylvester_hadamard():
+    """H_n H_n^T = n I with +/-1 entries; H_4's rows are the paper's c_n = 4 basis with the garbled
+    duplicate row replaced by [1, -1, 1, -1] (reading R11)."""
+    for n in (1, 2, 4, 8):
+        H = conv.hadamard(n)
+        assert set(np.unique(H)) <= {-1, 1}
+        assert np.array_equal(H @ H.T, n * np.eye(n, dtype=np.int64))
+    rows = {tuple(r) for r in conv.hadamard(4)}
+    assert rows == {(1, 1, 1, 1), (1, -1, 1, -1), (1, 1, -1, -1), (1, -1, -1, 1)}
+
+
+def test_hadamard_row_plaintexts_decode_to_patterns():
+    """The row-r plaintexts hold H_4[r][c] in every slot of group c (decoding = evaluation)."""
+    from oracle.encoding import decode
+    N = 64
+    P = bfv.BFVParams(N, ntt_primes(N, 50, 2), 65537)
+    p = conv.plan(N, 1, 4, 4, 2, 2, 3, 3, 1, False, 4)
+    H = conv.hadamard(4)
+    polys = conv.hadamard_row_polys(P, p)
+    for r in (1, 2, 3):
+        q = P.primes[0]
+        m = [conv.centered(int(x) if int(x) < q // 2 else int(x) - q, 65537) for x in polys[r - 1][0]]
+        slots = decode(np.mod(np.array(m, dtype=np.int64), 65537), 65537, N)
+        for c in range(4):
+            b = conv._group_base(p, c)
+            assert set(slots[b:b + N // 4].tolist()) == {H[r][c] % 65537}
+
+
+@pytest.mark.parametrize("w", [0, 20])
+def test_cn4_toy_decrypts_to_plain_conv(w):
+    """decrypt(HE-conv(enc x)) * 4^{-1} = plain conv mod t with 4 channels per ciphertext, for
+    the one-digit-per-limb gadget and a 2^20 sub-digit base."""
+    lay = make_layer(64, ntt_primes(64, 50, 3), batch=1, Ci=8, Co=5, H=2, W=2, kh=3, kw=3, pad=1,
+                     xrange=(-128, 128), wrange=(-128, 128), seed=71, force_cn=4, w=w)
+    assert (lay.plan.cn, lay.plan.J, lay.plan.Jout, lay.ls.scale) == (4, 2, 2, 4)
+    out = conv.he_conv(lay.P, lay.ls, lay.W, lay.ct_in, lay.keys)
+    check_decrypted(lay, out)
+
+
+def test_c1_in_one_ciphertext():
+    """BASELINE configs[0] (C1) packed as ONE ciphertext (c_n = 4; reading R19 superseded): needs the
+    sub-digit base for noise (dense Hadamard-row plaintexts multiply the key-switching noise by up
+    to N t / 2); with w = 20 it decrypts exactly with >= 4 bits of margin."""
+    cfg = synth.configs()["C1"]
+    lay = make_layer(cfg.N, cfg.primes, cfg.batch, cfg.Ci, cfg.Co, cfg.H, cfg.W, cfg.kh, cfg.kw, cfg.pad,
+                     seed=cfg.index, force_cn=4, x=synth.gen_image(cfg), Wt=synth.gen_weights(cfg), w=20)
+    assert (lay.plan.J, lay.plan.Jout) == (1, 1)
+    out = conv.he_conv(lay.P, lay.ls, lay.W, lay.ct_in, lay.keys)
+    check_decrypted(lay, out)
+    budget = bfv.noise_budget_bits(lay.P)
+    for ct in out.values():
+        assert budget - bfv.noise_bits(lay.P, ct, lay.s, bfv.decrypt(lay.P, ct, lay.s)) >= 4
+
+
+def test_c1_one_ciphertext_fails_without_subdigits():
+    """Negative control for the decomposition base: with one digit per 50-bit limb the c_n = 4 C1
+    layer's noise reaches Delta/2 and decryption is wrong (why NEXT-4's smaller base is needed)."""
+    cfg = synth.configs()["C1"]
+    lay = make_layer(cfg.N, cfg.primes, cfg.batch, cfg.Ci, cfg.Co, cfg.H, cfg.W, cfg.kh, cfg.kw, cfg.pad,
+                     seed=cfg.index, force_cn=4, x=synth.gen_image(cfg), Wt=synth.gen_weights(cfg), w=0)
+    out = conv.he_conv(lay.P, lay.ls, lay.W, lay.ct_in, lay.keys)
+    with pytest.raises(AssertionError):
+        check_decrypted(lay, out)

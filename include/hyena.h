@@ -50,7 +50,9 @@ typedef struct hy_weights hy_weights;
  * out[b,o,y,x] = sum_{c,dy,dx} W[o,c,dy,dx] x[b,c,y+dy-pad,x+dx-pad].
  * depthwise != 0: W is [C][kh][kw] and output channel o reads input channel o only.
  * k = 0 selects the paper's k (argmin_{1<=k<=32} |[k h]_t|; reading R13);
- * force_cn = 0 chooses c_n automatically (reading R10), else 1 or 2. */
+ * force_cn = 0 chooses c_n automatically (reading R10), else 1, 2 or 4 (4: four channels per
+ * ciphertext, Walsh-Hadamard-4 packing of PAPER.md:565-572; one unit of N/4-slot groups, dense layers,
+ * FP64 MAC paths, output scale 4). */
 typedef struct {
   uint32_t Ci, Co, H, W, kh, kw, pad, stride, depthwise, batch;
   int32_t k, force_cn;
@@ -79,6 +81,35 @@ typedef struct {
   uint32_t galois[HY_MAX_GALOIS];
 } hy_layout;
 
+/* Storage / communication accounting of a layer (Table 2 :833-872,
+ * Table 3 :917-919, storage example :561-562).  Byte counts use 8-byte words and L limbs.
+ *   input_ct_bytes / output_ct_bytes: this layout's J / Jout ciphertexts (2 L N words each): what
+ *       the client sends and receives;
+ *   input_ct_bytes_paper: the paper's count ceil(Ci Wp Hp / (N / ... )) = ceil(Ci Wp^2 / N)
+ *       ciphertexts (channels packed back to back, no halo rows);
+ *   model_bytes_paper: the proposed method's model, one 64-bit integer per kernel element
+ *       (PAPER.md:557-562), plus one N-word sign plaintext when c_n = 2 (the :561 example) or three
+ *       dense Hadamard-row plaintexts when c_n = 4;
+ *   model_bytes_conventional: one N-word plaintext per kernel element;
+ *   model_bytes_device: what hy_encode_weights keeps on the GPU for the weights (int8 + FP64 tables,
+ *       sign / Hadamard-row plaintexts in NTT form with Shoup companions);
+ *   key_bytes: the n_keys switching keys (ND x 2 x L x N words each, coefficient form);
+ *   rotations: hoisted rotations per evaluation (input cts x non-identity taps) plus alignment
+ *       rotations (c_n = 2: one per output ct; c_n = 4: three);
+ *   coef_macs: coefficient-level multiply-accumulates of the lazy MAC (S3). */
+typedef struct {
+  uint64_t input_ct_bytes, output_ct_bytes, input_ct_bytes_paper;
+  uint64_t model_bytes_paper, model_bytes_conventional, model_bytes_device;
+  uint64_t key_bytes;
+  uint32_t n_keys, rotations;
+  uint64_t coef_macs;
+} hy_accounting;
+
+/* Host-only: accounting of a planned layout (hy_plan_layout) for L limbs and ND key digits
+ * (ND = L, or L V with a sub-digit base).  Errors: HY_EINVAL. */
+hy_status hy_layout_accounting(const hy_layout* lay, const hy_conv_shape* shape, uint32_t L, uint32_t ND,
+                               hy_accounting* out);
+
 /* Thread-local message describing the last failing call ("" if none). */
 const char* hy_last_error(void);
 
@@ -96,10 +127,20 @@ hy_status hy_plan_layout(uint32_t N, uint64_t t, const hy_conv_shape* shape, hy_
  * Errors: HY_EINVAL, HY_ENOMEM, HY_ECUDA.  *out is set only on success. */
 hy_status hy_params_create(uint32_t N, const uint64_t* q_primes, uint32_t L, uint64_t t, int device,
                            hy_params** out);
+/* Same, with a decomposition base 2^w_dcmp INSIDE each RNS limb for the switching keys (SURVEY §8(f)
+ * NEXT-4; PAPER.md:1470 [app] "decomposition base"; smaller digits = less key-switching noise, e.g.
+ * for the dense Hadamard-row plaintexts of c_n = 4): w_dcmp = 0 is hy_params_create (one digit per
+ * limb, reading R5); else 4 <= w_dcmp < bit length of the smallest q_l, and every key has
+ * ND = L ceil(max bits / w_dcmp) digits, digit i V + v = floor([c1]_{q_i} / 2^{w v}) mod 2^w with
+ * gadget residue [i == l] 2^{w v} mod q_l (the oracle's bfv.galois_keygen).  The tensor-core fused
+ * MAC (one digit per limb) is not used with a sub-digit base.  Errors as hy_params_create. */
+hy_status hy_params_create2(uint32_t N, const uint64_t* q_primes, uint32_t L, uint64_t t, uint32_t w_dcmp, int device,
+                            hy_params** out);
 void hy_params_destroy(hy_params* p);
 
 /* Upload server-side switching keys generated by the client (PAPER.md:883-884, 1474-1475 [app]).
- * keys: [n_elts][L digits][2: b, a][L limbs][N] uint64, COEFFICIENT form, canonical residues;
+ * keys: [n_elts][ND digits][2: b, a][L limbs][N] uint64, COEFFICIENT form, canonical residues
+ * (ND = L, or L V with a sub-digit base: hy_params_create2);
  * key for element g satisfies b_{i,l} + a_{i,l} s = e_i + [i == l] s(X^g)  (mod q_l)
  * (RNS-digit gadget, reading R5).  keys_on_device != 0: `keys` is a device pointer.
  * The library converts them to NTT form with Shoup companions and keeps its own copy;

@@ -153,7 +153,8 @@ extern "C" hy_status hy_plan_layout(uint32_t N, uint64_t t, const hy_conv_shape*
            "empty shape");
   HY_CHECK(sh->depthwise || sh->Co >= 1, HY_ESHAPE, "Co must be >= 1");
   HY_CHECK(!sh->depthwise || sh->Co == sh->Ci || sh->Co == 0, HY_ESHAPE, "depthwise needs Co == Ci");
-  HY_CHECK(sh->force_cn == 0 || sh->force_cn == 1 || sh->force_cn == 2, HY_EINVAL, "force_cn must be 0, 1 or 2");
+  HY_CHECK(sh->force_cn == 0 || sh->force_cn == 1 || sh->force_cn == 2 || sh->force_cn == 4, HY_EINVAL,
+           "force_cn must be 0, 1, 2 or 4");
   hy_layout L;
   memset(&L, 0, sizeof(L));
   L.N = N;
@@ -168,6 +169,10 @@ extern "C" hy_status hy_plan_layout(uint32_t N, uint64_t t, const hy_conv_shape*
   if ((u64)L.Hp * L.Wp <= row) {
     L.mode = 0;
     L.per_row = row / (L.Hp * L.Wp);
+    if (sh->force_cn == 4) {  // c_n = 4: a channel's slot group is half a slot row (N/4 slots)
+      HY_CHECK((u64)L.Hp * L.Wp <= row / 2, HY_ESHAPE, "c_n = 4 needs an image block within N/4 slots");
+      L.per_row = (row / 2) / (L.Hp * L.Wp);
+    }
     L.bands = 1;
     L.G = (sh->batch + L.per_row - 1) / L.per_row;
   } else {
@@ -181,7 +186,13 @@ extern "C" hy_status hy_plan_layout(uint32_t N, uint64_t t, const hy_conv_shape*
   }
   L.cn = sh->force_cn ? (uint32_t)sh->force_cn : (L.G <= 1 ? 2u : 1u);
   const uint32_t C = sh->Ci;
-  if (L.cn == 2) {
+  if (L.cn == 4) {  // NEXT-1: 4 channels per ciphertext in slot groups c = 2 h + r (row r, half h)
+    HY_CHECK(L.mode == 0 && L.G == 1, HY_ESHAPE, "c_n = 4 needs the whole batch in one group of N/4 slots");
+    HY_CHECK(!sh->depthwise, HY_ESHAPE, "c_n = 4 is not supported for depthwise layers");
+    L.U = 1;
+    L.Jc = (C + 3) / 4;
+    L.Jo = (sh->Co + 3) / 4;
+  } else if (L.cn == 2) {
     L.U = L.G;
     L.Jc = (C + 1) / 2;
     L.Jo = sh->depthwise ? L.Jc : (sh->Co + 1) / 2;
@@ -233,7 +244,7 @@ extern "C" hy_status hy_plan_layout(uint32_t N, uint64_t t, const hy_conv_shape*
     L.sign_coeff = (int32_t)centered(mulmod(k, h, t), t);
   } else {
     L.k = 1;
-    L.scale = 1;
+    L.scale = L.cn == 4 ? 4 : 1;  // c_n = 4: H4 H4^T = 4 I (no k: the dense rows have no small multiple)
     L.sign_coeff = 0;
   }
   // Galois elements: left rotation by s <-> X -> X^{3^{s mod N/2}} (reading R7)
@@ -248,11 +259,50 @@ extern "C" hy_status hy_plan_layout(uint32_t N, uint64_t t, const hy_conv_shape*
     if (st != 0) add_g((uint32_t)powmod(3, (u64)st, 2 * (u64)N));
   }
   if (L.cn == 2 && !sh->depthwise) add_g(2 * N - 1);
+  if (L.cn == 4) {  // alignment of diagonal d: row swap^(d & 1) x half-row rotation^(d >> 1)
+    const u64 M2 = 2 * (u64)N, half_rot = powmod(3, N / 4, M2);
+    add_g(2 * N - 1);
+    add_g((uint32_t)half_rot);
+    add_g((uint32_t)mulmod(2 * N - 1, half_rot, M2));
+  }
   // exactness bounds of the FP64-pipe accumulation
   const u64 K = sh->depthwise ? L.n_taps : (u64)L.Jc * L.n_taps;
   HY_CHECK(K <= 65536, HY_ESHAPE, "MAC depth %llu exceeds 2^16", (unsigned long long)K);
-  HY_CHECK(L.cn == 1 || K * L.k <= (1u << 21), HY_ESHAPE, "MAC depth x k too large for exact accumulation");
+  HY_CHECK(L.cn != 2 || K * L.k <= (1u << 21), HY_ESHAPE, "MAC depth x k too large for exact accumulation");
   *out = L;
+  return HY_OK;
+}
+
+extern "C" hy_status hy_layout_accounting(const hy_layout* lay, const hy_conv_shape* sh, uint32_t L, uint32_t ND,
+                                          hy_accounting* out) {
+  HY_CHECK(lay && sh && out && L >= 1 && ND >= L, HY_EINVAL, "bad accounting arguments");
+  const u64 N = lay->N, ctb = 2 * (u64)L * N * 8;
+  const bool dw = sh->depthwise != 0;
+  const u64 Co = dw ? sh->Ci : sh->Co, T = lay->n_taps;
+  const u64 elems = dw ? (u64)sh->Ci * T : (u64)sh->Ci * Co * T;  // kernel elements
+  hy_accounting a;
+  memset(&a, 0, sizeof(a));
+  a.input_ct_bytes = (u64)lay->J * ctb;
+  a.output_ct_bytes = (u64)lay->Jout * ctb;
+  a.input_ct_bytes_paper = (((u64)sh->Ci * lay->Wp * lay->Hp + N - 1) / N) * ctb;
+  const u64 plaintexts = lay->cn == 4 ? 3 : lay->cn == 2 ? 1 : 0;
+  a.model_bytes_paper = elems * 8 + plaintexts * N * 8;
+  a.model_bytes_conventional = elems * N * 8;
+  // device copy (hy_encode_weights): int8 tiles + FP64 table over the padded MAC geometry, term
+  // table, plaintexts in NTT form with Shoup companions
+  const u64 M = dw ? (lay->cn == 2 ? 2 : 1) : (lay->cn == 4 ? 16 * (u64)lay->Jo : lay->cn == 2 ? 4 * (u64)lay->Jo : lay->Jo);
+  const u64 K = dw ? T : (u64)lay->Jc * T, wblocks = dw ? lay->Jc : 1;
+  const u64 Mpad = (u64)hy_mac_mpad((int)M, dw), Kpad = (K + 31) / 32 * 32;
+  a.model_bytes_device = wblocks * Kpad * Mpad * 8 + wblocks * ((Mpad + 127) / 128) * Kpad * 128 +
+                         (Kpad + 63) / 64 * 64 * 4 + plaintexts * 2 * (u64)L * N * 8;
+  a.n_keys = lay->n_galois;
+  a.key_bytes = (u64)lay->n_galois * ND * 2 * L * N * 8;
+  u64 ntap = 0;
+  for (uint32_t t = 0; t < lay->n_taps; t++)
+    if (((int64_t)lay->tap_step[t] % (int64_t)(N / 2)) != 0) ntap++;
+  a.rotations = (uint32_t)((u64)lay->J * ntap + (dw ? 0 : (lay->cn == 4 ? 3 : lay->cn == 2 ? 1 : 0)) * (u64)lay->Jout);
+  a.coef_macs = (dw ? (u64)lay->U * lay->Jc : lay->U) * M * K * 2 * L * N;
+  *out = a;
   return HY_OK;
 }
 
@@ -267,6 +317,11 @@ static hy_status upload(void** dst, const void* src, size_t bytes) {
 
 extern "C" hy_status hy_params_create(uint32_t N, const uint64_t* q, uint32_t L, uint64_t t, int device,
                                       hy_params** out) {
+  return hy_params_create2(N, q, L, t, 0, device, out);
+}
+
+extern "C" hy_status hy_params_create2(uint32_t N, const uint64_t* q, uint32_t L, uint64_t t, uint32_t w_dcmp,
+                                       int device, hy_params** out) {
   HY_CHECK(out && q, HY_EINVAL, "null argument");
   HY_CHECK(N >= 1024 && N <= 16384 && (N & (N - 1)) == 0, HY_EINVAL, "N=%u must be a power of two in [1024, 16384]",
            N);
@@ -279,8 +334,22 @@ extern "C" hy_status hy_params_create(uint32_t N, const uint64_t* q, uint32_t L,
     HY_CHECK(q[l] != t, HY_EINVAL, "q[%u] equals t", l);
     for (uint32_t m = 0; m < l; m++) HY_CHECK(q[m] != q[l], HY_EINVAL, "duplicate prime");
   }
+  uint32_t qbits_max = 0, qbits_min = 64;
+  for (uint32_t l = 0; l < L; l++) {
+    uint32_t b = 0;
+    while (b < 64 && (q[l] >> b)) b++;
+    qbits_max = std::max(qbits_max, b);
+    qbits_min = std::min(qbits_min, b);
+  }
+  HY_CHECK(w_dcmp == 0 || (w_dcmp >= 4 && w_dcmp < qbits_min), HY_EINVAL,
+           "decomposition base 2^%u: w must be 0 or in [4, %u)", w_dcmp, qbits_min);
+  const uint32_t V = w_dcmp ? (qbits_max + w_dcmp - 1) / w_dcmp : 1;
+  HY_CHECK(L * V <= 4 * HY_MAX_LIMBS, HY_EINVAL, "too many gadget digits (%u)", L * V);
   HY_CUDA_TRY(cudaSetDevice(device));
   hy_params* p = new hy_params();
+  p->w_dcmp = w_dcmp;
+  p->V = V;
+  p->ND = L * V;
   p->N = N;
   p->logN = 0;
   while ((1u << p->logN) < N) p->logN++;
@@ -391,7 +460,7 @@ extern "C" hy_status hy_keys_upload(hy_params* p, uint32_t n, const uint32_t* el
   HY_CHECK(p && (n == 0 || (elts && keys)), HY_EINVAL, "null argument");
   HY_CUDA_TRY(cudaSetDevice(p->device));
   const size_t L = p->L, N = p->N;
-  const size_t key_words = L * 2 * L * N;
+  const size_t key_words = (size_t)p->ND * 2 * L * N;
   u64* tmp = nullptr;
   HY_CUDA_TRY(cudaMalloc(&tmp, key_words * sizeof(u64)));
   for (uint32_t e = 0; e < n; e++) {
@@ -447,9 +516,86 @@ extern "C" hy_status hy_keys_upload(hy_params* p, uint32_t n, const uint32_t* el
 // ============================================================================================
 // weights
 // ============================================================================================
+namespace {
+// host negacyclic transforms mod t (t < 2^32): forward out[k] = m(zeta^{2 bitrev(k) + 1}) (Cooley-Tukey),
+// inverse = its exact inverse (Gentleman-Sande with zeta^{-1} and the N^{-1} scaling)
+void host_ntt_t(std::vector<u64>& a, u64 t, u64 zeta, uint32_t logN);
+void host_intt_t(std::vector<u64>& a, u64 t, u64 zeta, uint32_t logN) {
+  const uint32_t N = 1u << logN;
+  const u64 zi = invmod(zeta, t);
+  std::vector<u64> zr(N);
+  for (uint32_t k = 0; k < N; k++) zr[k] = powmod(zi, bitrev(k, logN), t);
+  for (uint32_t m = N / 2, tt = 1; m >= 1; m /= 2, tt *= 2)
+    for (uint32_t i = 0; i < m; i++) {
+      const u64 w = zr[m + i];
+      for (uint32_t j = 2 * i * tt; j < 2 * i * tt + tt; j++) {
+        const u64 U = a[j], V = a[j + tt];
+        a[j] = (U + V) % t;
+        a[j + tt] = (U + t - V) % t * w % t;
+      }
+    }
+  const u64 ni = invmod(N % t, t);
+  for (auto& x : a) x = x * ni % t;
+}
+}  // namespace
+
+// c_n = 4 (NEXT-1, Sylvester basis, reading R11): the plaintexts of Walsh-Hadamard
+// rows r = 1..3, slot group c = 2 h + r' (slot row r', half h of the row) holding H4[r][c] =
+// (-1)^{popcount(r & c)}; encoded mod t on the host (inverse transform), self-checked by the forward
+// transform, centered-lifted into every limb (R14), NTT'd with Shoup companions: [3][2][L][N].
+static hy_status hadamard_rows(hy_params* p, const hy_layout& lay, u64** out) {
+  (void)lay;
+  const uint32_t N = p->N, L = p->L, half = N / 2;
+  const u64 t = p->t;
+  std::vector<u64> host((size_t)3 * L * N);
+  for (int r = 1; r < 4; r++) {
+    std::vector<u64> a(N);
+    std::vector<int> pat(N);
+    u64 e = 1;
+    for (uint32_t i = 0; i < half; i++) {
+      for (int row = 0; row < 2; row++) {
+        const u64 ex = row ? 2 * (u64)N - e : e;
+        const uint32_t k = bitrev((uint32_t)((ex - 1) / 2), p->logN);
+        const int c = 2 * (i >= half / 2 ? 1 : 0) + row;
+        const int sgn = __builtin_popcount(r & c) & 1 ? -1 : 1;
+        a[k] = sgn > 0 ? 1 : t - 1;
+        pat[k] = sgn;
+      }
+      e = e * 3 % (2 * (u64)N);
+    }
+    std::vector<u64> m = a;
+    host_intt_t(m, t, p->zeta_t, p->logN);
+    std::vector<u64> chk = m;
+    host_ntt_t(chk, t, p->zeta_t, p->logN);
+    for (uint32_t k = 0; k < N; k++)
+      HY_CHECK(chk[k] == a[k], HY_EINVAL, "Hadamard-row plaintext self-check failed (row %d)", r);
+    for (uint32_t l = 0; l < L; l++)
+      for (uint32_t k = 0; k < N; k++) {
+        const int64_t cen = centered(m[k], t);
+        host[((size_t)(r - 1) * L + l) * N + k] = cen >= 0 ? (u64)cen % p->q[l] : p->q[l] - ((u64)(-cen) % p->q[l]);
+      }
+  }
+  u64* tmp = nullptr;
+  hy_status st = upload((void**)&tmp, host.data(), host.size() * sizeof(u64));
+  if (st != HY_OK) return st;
+  if (cudaMalloc(out, (size_t)3 * 2 * L * N * sizeof(u64)) != cudaSuccess) {
+    *out = nullptr;
+    cudaFree(tmp);
+    hy_set_error("Hadamard-row plaintext allocation failed");
+    return HY_ENOMEM;
+  }
+  for (int r = 0; r < 3 && st == HY_OK; r++) {
+    u64* dst = *out + (size_t)r * 2 * L * N;
+    st = hyk::ntt_poly_fwd(p, tmp + (size_t)r * L * N, dst, 1, 0);
+    if (st == HY_OK) st = hyk::shoup_table(p, dst, dst + (size_t)L * N, 1, 0);
+  }
+  cudaDeviceSynchronize();
+  cudaFree(tmp);
+  return st;
+}
 // 1x1 kernel, no padding, dense: the coefficient-domain MAC applies (HY_MAC_TC_COEF)
 static bool coef_ok(const hy_weights* w, const hy_layout& lay) {
-  return !w->shape.depthwise && lay.n_taps == 1 && lay.tap_step[0] == 0;
+  return !w->shape.depthwise && lay.cn <= 2 && lay.n_taps == 1 && lay.tap_step[0] == 0;
 }
 
 extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, const int8_t* Wt, hy_weights** out) {
@@ -470,12 +616,13 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
     w->K = T;
     w->wblocks = (int)lay.Jc;
   } else {
-    w->M = lay.cn == 2 ? (int)(4 * lay.Jo) : (int)lay.Jo;
+    // MAC rows per output ct: c_n = 2: (diagonal d, slot row c); c_n = 4: (diagonal d, slot group c)
+    w->M = lay.cn == 4 ? (int)(16 * lay.Jo) : lay.cn == 2 ? (int)(4 * lay.Jo) : (int)lay.Jo;
     w->K = (int)lay.Jc * T;
     w->wblocks = 1;
   }
   w->Mpad = hy_mac_mpad(w->M, dw);
-  w->mac_path = hy_mac_path(w->M, (int)p->L, dw, coef_ok(w, lay));
+  w->mac_path = hy_mac_path(w->M, (int)p->L, dw, coef_ok(w, lay), (int)lay.cn, p->ND != p->L);
   w->Kpad = (w->K + 31) / 32 * 32;  // multiple of the MAC K chunks (16 FP64 GEMM, 32 tcgen05)
   // weight table (S0), [block][kk][row] as exact doubles; row semantics documented in DESIGN.md §4
   std::vector<double> wt((size_t)w->wblocks * w->Kpad * w->Mpad, 0.0);
@@ -492,6 +639,11 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
         int32_t v;
         if (dw) {
           v = lay.cn == 2 ? Wat(2 * b + row, 2 * b + row, kk) : Wat(b, b, kk);
+        } else if (lay.cn == 4) {
+          // row = (g*4 + d)*4 + c : slot group c of diagonal d pairs input 4j+c with output 4g+(c^d)
+          const int g = row / 16, d = (row / 4) % 4, c = row % 4;
+          const int tau = kk / (int)lay.Jc, j = kk % (int)lay.Jc;
+          v = Wat(4 * g + (c ^ d), 4 * j + c, tau);
         } else if (lay.cn == 2) {
           // row = (g*2 + d)*2 + c : slot row c of diagonal d pairs input 2j+c with output 2g+(c^d)
           const int g = row / 4, d = (row / 2) % 2, c = row % 2;
@@ -530,6 +682,10 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
   }
   const size_t L = p->L, N = p->N, ctw = 2 * L * N;
   const size_t Jin = (size_t)lay.U * lay.Jc, Jo = (size_t)lay.U * lay.Jo;
+  if (lay.cn == 4 && (st = hadamard_rows(p, lay, &w->d_sign)) != HY_OK) {
+    hy_weights_destroy(w);
+    return st;
+  }
   // sign plaintext [k,-k]: [k h]_t at X^{N/4}, X^{3N/4}, centered lift (R14)
   if (lay.cn == 2) {
     std::vector<u64> sp(L * N, 0);
@@ -568,15 +724,17 @@ extern "C" hy_status hy_encode_weights(hy_params* p, const hy_conv_shape* sh, co
     if (ru < 1) ru = 1;
     w->r_units = (int)std::min<size_t>(ru, lay.U);
   }
+  const size_t ND = p->ND;
+  const bool align = lay.cn >= 2 && !dw;  // partial sums aligned by HRot (S4)
   struct A {
     u64** ptr;
     size_t words;
   } allocs[] = {
-      {&w->d_D, std::max(Jin, (lay.cn == 2 && w->mac_path == HY_MAC_TC_COEF) ? Jo : 0) * L * L * N},
+      {&w->d_D, std::max(Jin, (lay.cn == 2 && w->mac_path == HY_MAC_TC_COEF) ? Jo : 0) * ND * L * N},
       {&w->d_C0, std::max(Jin, (lay.cn == 2 && w->mac_path == HY_MAC_TC_COEF) ? Jo : 0) * L * N},
-      {&w->d_P, Jo * ctw * ((lay.cn == 2 && !dw) ? 2 : 1)},
-      {&w->d_D2, (lay.cn == 2 && !dw) ? Jo * L * L * N + Jo * L * N : 0},
-      {&w->d_X, (lay.cn == 2 && !dw) ? Jo * ctw : 0},
+      {&w->d_P, Jo * ctw * (lay.cn == 4 ? 4 : (lay.cn == 2 && !dw) ? 2 : 1)},
+      {&w->d_D2, align ? Jo * ND * L * N + Jo * L * N : 0},
+      {&w->d_X, align ? Jo * ctw : 0},
       {&w->d_A1, (lay.cn == 2 && w->mac_path == HY_MAC_TC_COEF) ? Jo * 2 * ctw : 0},
       {&w->d_R, (w->mac_path == HY_MAC_TC_SPLIT || w->mac_path == HY_MAC_FP64_SPLIT)
                     ? (size_t)w->r_units * w->K * ctw : 0},
@@ -636,10 +794,11 @@ extern "C" hy_status hy_weights_set_mac_path(hy_weights* w, int32_t path) {
   const bool dw = w->shape.depthwise != 0;
   const int L = (int)w->p->L;
   bool ok = false;
+  const bool cn4 = w->lay.cn == 4, sub = w->p->ND != w->p->L;
   switch (path) {
     case HY_MAC_THIN: ok = dw; break;
-    case HY_MAC_TC_FUSED: ok = !dw && w->M <= 128 && (L == 2 || L == 3 || L == 5); break;
-    case HY_MAC_TC_SPLIT: ok = !dw; break;
+    case HY_MAC_TC_FUSED: ok = !dw && !cn4 && !sub && w->M <= 128 && (L == 2 || L == 3 || L == 5); break;
+    case HY_MAC_TC_SPLIT: ok = !dw && !cn4; break;
     case HY_MAC_FP64_SPLIT: ok = !dw && w->M > 32; break;  // 64-row FP64 tiles (hy_mac_mpad)
     case HY_MAC_FP64_FUSED: ok = !dw && w->M <= 32; break;
     case HY_MAC_TC_COEF: ok = coef_ok(w, w->lay); break;
@@ -657,7 +816,7 @@ extern "C" hy_status hy_weights_set_mac_path(hy_weights* w, int32_t path) {
     }
     if (Jo > Jin) {  // allocate the larger digit workspaces first: on failure the old ones stay valid
       u64 *nd = nullptr, *nc = nullptr;
-      if (cudaMalloc(&nd, Jo * L * L * N * sizeof(u64)) != cudaSuccess ||
+      if (cudaMalloc(&nd, Jo * w->p->ND * L * N * sizeof(u64)) != cudaSuccess ||
           cudaMalloc(&nc, Jo * L * N * sizeof(u64)) != cudaSuccess) {
         cudaFree(nd);
         hy_set_error("coefficient-domain digit workspace allocation failed");
@@ -743,6 +902,18 @@ static hy_status bind_keys(hy_weights* w) {
     auto it = p->keys.find(2 * p->N - 1);
     HY_CHECK(it != p->keys.end(), HY_ENOKEY, "no Galois key for the row swap (element %u)", 2 * p->N - 1);
     w->d_swap_key = it->second.ntt;
+  }
+  if (lay.cn == 4) {  // the last three layout elements: alignment of diagonals 1, 2, 3
+    for (int d = 0; d < 3; d++) {
+      const uint32_t g = d == 0 ? 2 * p->N - 1
+                                : d == 1 ? (uint32_t)powmod(3, p->N / 4, 2 * (u64)p->N)
+                                         : (uint32_t)mulmod(2 * p->N - 1, powmod(3, p->N / 4, 2 * (u64)p->N),
+                                                            2 * (u64)p->N);
+      auto it = p->keys.find(g);
+      HY_CHECK(it != p->keys.end(), HY_ENOKEY, "no Galois key for the c_n = 4 alignment (element %u)", g);
+      w->d_align_key[d] = it->second.ntt;
+      HY_CHECK(hy_galois_act(g, p->N, &w->h_align_act[d]), HY_EINVAL, "bad Galois element %u", g);
+    }
   }
   for (uint32_t tau = 0; tau < lay.n_taps; tau++) {
     w->h_tap_keys[tau] = ptrs[tau];
@@ -890,7 +1061,7 @@ extern "C" hy_status hy_rotate(hy_params* p, const uint64_t* ct_in, uint32_t g, 
   u64* work = nullptr;
   GaloisAct act;
   HY_CHECK(hy_galois_act(g, p->N, &act), HY_EINVAL, "Galois element %u is not odd / < 2N", g);
-  HY_CUDA_TRY(cudaMalloc(&work, n * (p->L * p->L + 3 * p->L) * p->N * sizeof(u64)));
+  HY_CUDA_TRY(cudaMalloc(&work, n * (p->ND * p->L + 3 * p->L) * p->N * sizeof(u64)));
   hy_status st = hyk::rotate_ct(p, ct_in, act, it->second.ntt, ct_out, n, work, s);
   cudaError_t ce = cudaStreamSynchronize(s);
   cudaFree(work);
@@ -929,15 +1100,15 @@ extern "C" hy_status hy_keygen(hy_params* p, uint64_t seed, uint32_t n, const ui
   for (uint32_t e = 0; e < n; e++)
     HY_CHECK((elts[e] & 1) && elts[e] < 2 * p->N, HY_EINVAL, "Galois element %u must be odd and < 2N", elts[e]);
   HY_CUDA_TRY(cudaSetDevice(p->device));
-  const size_t L = p->L, N = p->N, kw = L * 2 * L * N;
+  const size_t L = p->L, N = p->N, ND = p->ND, kw = ND * 2 * L * N;
   DevBuf sres, s8, sntt, del, work, kout;
   HY_CUDA_TRY(cudaMalloc(&sres.p, L * N * 8));
   HY_CUDA_TRY(cudaMalloc(&s8.p, N));
   HY_CUDA_TRY(cudaMalloc(&sntt.p, 2 * L * N * 8));
   HY_CUDA_TRY(cudaMalloc(&del.p, n * sizeof(uint32_t)));
   HY_CUDA_TRY(cudaMemcpy(del.p, elts, n * sizeof(uint32_t), cudaMemcpyHostToDevice));
-  // work: A, NTT(A) [n L][L][N], s(X^g) [n][L][N], errors [n L][N] int32
-  HY_CUDA_TRY(cudaMalloc(&work.p, (2 * n * L * L * N + n * L * N) * 8 + n * L * N * 4));
+  // work: A, NTT(A) [n ND][L][N], s(X^g) [n][L][N], errors [n ND][N] int32
+  HY_CUDA_TRY(cudaMalloc(&work.p, (2 * n * ND * L * N + n * L * N) * 8 + n * ND * N * 4));
   u64* out = keys_out;
   if (!out) {
     HY_CUDA_TRY(cudaMalloc(&kout.p, n * kw * 8));

@@ -98,6 +98,9 @@ struct KeyEntry {
 
 struct hy_params {
   uint32_t N, logN, L;
+  uint32_t w_dcmp = 0;  // sub-digit decomposition base 2^w inside each limb (0: one digit per limb)
+  uint32_t V = 1;       // sub-digits per limb
+  uint32_t ND = 0;      // gadget digits L V: D is [ct][ND][L][N], a key [ND][2][L][N]
   u64 t;
   u64 q[HY_MAX_LIMBS];
   int device;
@@ -137,7 +140,7 @@ enum HyMacPath {
   HY_MAC_TC_COEF = 5,     // 1x1: tcgen05 MAC straight on the coefficient-form inputs (c_n = 1: no NTT;
                           // c_n = 2: only the row-swap alignment's NTTs)
 };
-int hy_mac_path(int M, int L, bool depthwise, bool coef_ok);
+int hy_mac_path(int M, int L, bool depthwise, bool coef_ok, int cn, bool subdigits);
 
 struct hy_weights {
   hy_params* p;
@@ -153,7 +156,8 @@ struct hy_weights {
                     // tensor-core MAC's term table (no integer division in its producers)
   int8_t* d_w8;     // [wblocks][Mpad/128][Kpad/32][4096]: weights as int8 in the tcgen05 K-major
                     // no-swizzle canonical layout (tensor-core MAC), zero padded
-  u64* d_sign;      // [L][N] NTT form of the [k,-k] plaintext, then [L][N] Shoup companions
+  u64* d_sign;      // [L][N] NTT form of the [k,-k] plaintext, then [L][N] Shoup companions (c_n = 4:
+                    // [3][2][L][N] for the dense Hadamard rows 1..3)
   // workspace (device)
   u64* d_D;         // [U*Jc][L digit][L limb][N] NTT-form digits
   u64* d_C0;        // [U*Jc][L][N]    NTT(c0)
@@ -172,6 +176,8 @@ struct hy_weights {
   GaloisAct h_tap_act[HY_MAX_TAPS];
   GaloisAct* d_tap_act;        // device array of slot-order automorphism actions per tap
   u64* d_swap_key;
+  u64* d_align_key[3];         // c_n = 4: keys of the alignment automorphisms g_1, g_2, g_3
+  GaloisAct h_align_act[3];
   u64 keys_version;            // params->keys_version the tap table was built from
   cudaEvent_t ev[4];           // optional stage-boundary events (bench)
   uint32_t n_ev;

@@ -45,7 +45,8 @@ struct PolyJob {  // src/dst [n][L][N]; `src_stride_polys` lets a job walk every
 };
 
 // S1 PermDecomp (PAPER.md:375-377, :1472 [app]): per input ct, digits d_i = [c1]_{q_i} lifted to
-// every limb l and NTT'd (L*L jobs), plus NTT(c0) per limb (L jobs).
+// every limb l and NTT'd (ND*L jobs), plus NTT(c0) per limb (L jobs).  With a sub-digit base 2^w
+// (hy_params_create2, NEXT-4) digit dd = i V + v is floor(d_i / 2^{w v}) mod 2^w (< 2^w < q_l).
 struct PermDecompJob {
   const u64* ct;
   u64* D;
@@ -58,19 +59,24 @@ struct PermDecompJob {
   u64* d;
   u64 qd;
   bool red;
+  int ND = 0, V = 1, wd = 0;  // gadget digits (0: ND = L), sub-digits per limb, base bits
+  int sh = -1;                 // sub-digit shift of this job (-1: a whole residue)
   __device__ void bind(int b) {
-    const int per = L * L + L;
+    const int nd = ND ? ND : L;
+    const int per = nd * L + L;
     const int c = b / per, r = b % per;
     const u64* cb = ct + (size_t)c * (ct_stride ? ct_stride : (size_t)2 * L * N);
-    if (r < L * L) {
-      const int i = r / L;
+    sh = -1;
+    if (r < nd * L) {
+      const int dd = r / L, i = dd / V;
       limb = r % L;
       s = cb + ((size_t)L + i) * N;
-      d = D + ((size_t)(c * L + i) * L + limb) * N;
+      d = D + ((size_t)(c * nd + dd) * L + limb) * N;
       qd = qa.q[limb];
-      red = qa.q[i] / 4 >= qa.q[limb];  // digit may exceed the lazy [0, 4 q_l) input range
+      if (V > 1) sh = wd * (dd % V);
+      red = V > 1 ? false : qa.q[i] / 4 >= qa.q[limb];  // digit may exceed the lazy [0, 4 q_l) range
     } else {
-      limb = r - L * L;
+      limb = r - nd * L;
       s = cb + (size_t)limb * N;
       d = C0 + ((size_t)c * L + limb) * N;
       qd = qa.q[limb];
@@ -79,6 +85,7 @@ struct PermDecompJob {
   }
   __device__ u64 load(int k) const {
     u64 x = s[k];
+    if (sh >= 0) return (x >> sh) & ((1ull << wd) - 1);
     return red ? x % qd : x;
   }
   __device__ void store(int k, u64 v) const { d[k] = v; }
@@ -103,10 +110,11 @@ struct StridedInvJob {
   __device__ void store(int k, u64 v) const { d[k] = v; }
 };
 
-// row-swap step (b): NTT_l of digit i (coefficient form, in [0, q_i)) for l != i
+// row-swap step (b): NTT_l of digit i (coefficient form, in [0, q_i)) for l != i (RNS digits: digit i
+// in limb i is the ct's own NTT(c1) limb i); with a sub-digit base every (digit dd, limb l) pair
 struct DigitLiftJob {
   const u64* dig;  // [o][L][N]
-  u64* D2;         // [o][L digit][L limb][N]
+  u64* D2;         // [o][ND digit][L limb][N]
   int L, N;
   QArr qa;
   int limb;
@@ -114,7 +122,21 @@ struct DigitLiftJob {
   u64* d;
   u64 qd;
   bool red;
+  int ND = 0, V = 1, wd = 0;
+  int sh = 0;
   __device__ void bind(int b) {
+    if (ND) {  // sub-digits: all ND * L jobs
+      const int per = ND * L;
+      const int o = b / per, r = b % per;
+      const int dd = r / L, i = dd / V;
+      limb = r % L;
+      s = dig + ((size_t)o * L + i) * N;
+      d = D2 + (((size_t)o * ND + dd) * L + limb) * N;
+      qd = qa.q[limb];
+      sh = wd * (dd % V);
+      red = false;
+      return;
+    }
     const int per = L * (L - 1);
     const int o = b / per, r = b % per;
     const int i = r / (L - 1), lj = r % (L - 1);
@@ -126,6 +148,7 @@ struct DigitLiftJob {
   }
   __device__ u64 load(int k) const {
     u64 x = s[k];
+    if (ND) return (x >> sh) & ((1ull << wd) - 1);
     return red ? x % qd : x;
   }
   __device__ void store(int k, u64 v) const { d[k] = v; }
@@ -151,6 +174,7 @@ struct KsApplyArgs {
   int L, logN;
   size_t total;  // nout * L * N
   LimbConsts lcs;
+  int ND = 0;    // gadget digits (0: ND = L, one per limb); D is [o][ND][L][N], keys [ND][2][L][N]
 };
 
 template <int LT>
@@ -159,6 +183,7 @@ __global__ void __launch_bounds__(256) ks_apply_kernel(KsApplyArgs a) {
   const size_t idx = (size_t)blockIdx.x * 256 + threadIdx.x;
   if (idx >= a.total) return;
   const int N = 1 << a.logN, L = LT > 0 ? LT : a.L;
+  const int ND = LT > 0 ? LT : (a.ND ? a.ND : a.L);
   const int j = (int)(idx & (N - 1));
   const size_t ol = idx >> a.logN;
   const int l = (int)(ol % L);
@@ -166,15 +191,13 @@ __global__ void __launch_bounds__(256) ks_apply_kernel(KsApplyArgs a) {
   const LimbConst& c = a.lcs.lc[l];
   const u64 q = c.q, q2 = c.two_q;
   const int jp = galois_perm(j, a.act, N >> 1);
-  const size_t LN = (size_t)L * N, kblk = 2 * L * LN;
+  const size_t LN = (size_t)L * N, kblk = 2 * ND * LN;
   const u64* D = a.D + o * a.D_stride;
   const u64* kb = a.key + (size_t)l * N + j;
   u64 a0 = __ldg(a.c0 + o * a.c0_stride + (size_t)l * N + jp), a1 = 0;
-#pragma unroll
-  for (int i = 0; i < (LT > 0 ? LT : HY_MAX_LIMBS); i++) {
-    if (LT == 0 && i >= L) break;
-    const u64 dv = (a.diag && i == l) ? __ldg(a.diag + o * a.diag_stride + (size_t)i * N + jp)
-                                      : __ldg(D + ((size_t)i * L + l) * N + jp);
+  for (int i = 0; i < ND; i++) {
+    const u64 dv = (a.diag && ND == L && i == l) ? __ldg(a.diag + o * a.diag_stride + (size_t)i * N + jp)
+                                                 : __ldg(D + ((size_t)i * L + l) * N + jp);
     const u64* k0 = kb + (size_t)(2 * i) * LN;
     const u64* k1 = k0 + LN;
     a0 = csub(a0 + shoup_mul(dv, __ldg(k0), __ldg(k0 + kblk), q), q2);
@@ -193,7 +216,7 @@ __global__ void __launch_bounds__(256) ks_apply_kernel(KsApplyArgs a) {
 hy_status launch_ks_apply(const KsApplyArgs& a, cudaStream_t s) {
   if (!a.total) return HY_OK;
   const unsigned blocks = (unsigned)((a.total + 255) / 256);
-  switch (a.L) {  // compile-time digit count: all loads of a thread issue at once
+  switch (a.ND && a.ND != a.L ? 0 : a.L) {  // compile-time digit count: all loads of a thread issue at once
     case 2: HY_CUDA_TRY(hy_launch(ks_apply_kernel<2>, dim3(blocks), dim3(256), 0, s, 1, a)); break;
     case 3: HY_CUDA_TRY(hy_launch(ks_apply_kernel<3>, dim3(blocks), dim3(256), 0, s, 1, a)); break;
     case 5: HY_CUDA_TRY(hy_launch(ks_apply_kernel<5>, dim3(blocks), dim3(256), 0, s, 1, a)); break;
@@ -446,7 +469,20 @@ struct KsMacArgs {
   int T, Jcb, K, Kpad, M, Mpad, wblocks, L, logN, kscale, cn;
   int dbg;                     // measurement experiments only (HY_DEBUG_KSMAC): 1 = skip the UMMAs
   LimbConsts lcs;
+  int ND, wd;                  // gadget digits per ct (D is [ct][ND][L][N]; ND = L: one per limb), base bits
+  int hr;                      // c_n = 4: sign holds the 3 dense Hadamard-row plaintexts [3][2][L][N]
 };
+
+// NTT_l(c1 limb l) of a ct from its digit block D [ND][L][N] (the identity tap's R.c1): digit l itself
+// with one digit per limb, else sum_v 2^{w v} NTT_l(d_{l,v}) (sub-digit base; generic kernels only)
+__device__ __forceinline__ u64 ident_c1(const u64* D, int L, int ND, int wd, size_t N, int l, int j, u64 q) {
+  if (ND == L) return __ldg(D + ((size_t)l * L + l) * N + j);
+  const int V = ND / L;
+  u64 acc = 0;
+  for (int v = 0; v < V; v++)
+    acc = (acc + mulmod_slow(__ldg(D + ((size_t)(l * V + v) * L + l) * N + j), (1ull << (wd * v)) % q, q)) % q;
+  return acc;
+}
 
 constexpr uint32_t M30 = 0x3FFFFFFFu;
 
@@ -498,16 +534,16 @@ __device__ __forceinline__ void ks_pair_regs(const u64* __restrict__ D, const u6
   r1 = csub(reduce_2q(a1, c.one_sh, q), q);
 }
 
-// generic (runtime L) version reading the key from global memory
+// generic (runtime L, ND digits) version reading the key from global memory
 __device__ __forceinline__ void ks_pair_any(const u64* __restrict__ D, const u64* __restrict__ C0,
                                             const u64* __restrict__ key, int L, int logN, int l, int j, int jp,
-                                            const LimbConst& c, u64& r0, u64& r1) {
+                                            const LimbConst& c, u64& r0, u64& r1, int ND) {
   const size_t N = (size_t)1 << logN;
-  const size_t LN = (size_t)L * N, kblk = 2 * L * LN;
+  const size_t LN = (size_t)L * N, kblk = 2 * ND * LN;
   const u64 q = c.q, q2 = c.two_q;
   u64 a0 = __ldg(C0 + (size_t)l * N + jp), a1 = 0;
   const u64* kb = key + (size_t)l * N + j;
-  for (int i = 0; i < L; i++) {
+  for (int i = 0; i < ND; i++) {
     const u64 dv = __ldg(D + ((size_t)i * L + l) * N + jp);
     const u64* k0 = kb + (size_t)(2 * i) * LN;
     const u64* k1 = k0 + LN;
@@ -524,16 +560,17 @@ __device__ __forceinline__ void r_value(const KsMacArgs& a, const u64* const* ke
                                         int kk, int l, int j, const LimbConst& c, KeyRegs<LT>& kr, u64& r0,
                                         u64& r1) {
   const int L = LT > 0 ? LT : a.L;
+  const int ND = LT > 0 ? LT : a.ND;
   const int N = 1 << a.logN;
   const size_t LN = (size_t)L * N;
   const int t = kk / a.Jcb, cc = kk - t * a.Jcb;
   const size_t ct = (size_t)z * a.Jcb + cc;
   const u64* C0 = a.C0 + ct * LN;
-  const u64* D = a.D + ct * L * LN;
+  const u64* D = a.D + ct * ND * LN;
   const u64* key = keys[t];
   if (key == nullptr) {
     r0 = __ldg(C0 + (size_t)l * N + j);
-    r1 = __ldg(D + ((size_t)l * L + l) * N + j);
+    r1 = ident_c1(D, L, ND, a.wd, N, l, j, c.q);
     return;
   }
   const int jp = galois_perm(j, act[t], N >> 1);
@@ -545,7 +582,7 @@ __device__ __forceinline__ void r_value(const KsMacArgs& a, const u64* const* ke
     }
     ks_pair_regs<LT>(D, C0, kr, a.logN, l, jp, c, r0, r1);
   } else {
-    ks_pair_any(D, C0, key, L, a.logN, l, j, jp, c, r0, r1);
+    ks_pair_any(D, C0, key, L, a.logN, l, j, jp, c, r0, r1, ND);
   }
 }
 
@@ -594,6 +631,31 @@ __device__ __forceinline__ void store_outputs(const KsMacArgs& a, int z, int row
       if (row + r < a.M)
         a.out[((size_t)(z * a.M + row + r) * 2 + comp) * LN + (size_t)l * N + j] =
             reduce_wide(__double2ll_rn(ah[r]), __double2ll_rn(al[r]), c);
+  } else if (a.cn == 4) {
+    // rows (g, d, c): slot group c's accumulator B_c of diagonal d.  Walsh-Hadamard-4 (Sylvester)
+    // on the exact accumulators, A_r = sum_c H4[r][c] B_c, ONE reduction each, then the PMults by the
+    // Hadamard-row plaintexts (row 0 = 1) and HAdd: P_{g,d} = A_0 + sum_{r >= 1} S_r A_r
+    // (PAPER.md:565-572 generalised; ProposedConv, PAPER.md:1536-1551 [ign])
+    for (int r0 = 0; r0 + 3 < nrows; r0 += 4) {
+      if (row + r0 >= a.M) break;
+      long long H[4], Lo[4];
+#pragma unroll
+      for (int cc = 0; cc < 4; cc++) {
+        H[cc] = __double2ll_rn(ah[r0 + cc]);
+        Lo[cc] = __double2ll_rn(al[r0 + cc]);
+      }
+      const long long AH[4] = {H[0] + H[1] + H[2] + H[3], H[0] - H[1] + H[2] - H[3], H[0] + H[1] - H[2] - H[3],
+                               H[0] - H[1] - H[2] + H[3]};
+      const long long AL[4] = {Lo[0] + Lo[1] + Lo[2] + Lo[3], Lo[0] - Lo[1] + Lo[2] - Lo[3],
+                               Lo[0] + Lo[1] - Lo[2] - Lo[3], Lo[0] - Lo[1] - Lo[2] + Lo[3]};
+      u64 v = reduce_wide(AH[0], AL[0], c);
+#pragma unroll
+      for (int r = 1; r < 4; r++) {
+        const u64* sr = a.sign + (size_t)(r - 1) * 2 * LN + (size_t)l * N + j;
+        v = csub(v + shoup_mul(reduce_wide(AH[r], AL[r], c), __ldg(sr), __ldg(sr + LN), c.q), c.two_q);
+      }
+      a.out[((size_t)(z * (a.M / 4) + (row + r0) / 4) * 2 + comp) * LN + (size_t)l * N + j] = csub(v, c.q);
+    }
   } else {
     const u64 sg = __ldg(a.sign + (size_t)l * N + j), sgs = __ldg(a.sign + LN + (size_t)l * N + j);
     const long long kk = a.kscale;
@@ -855,7 +917,7 @@ __global__ void __launch_bounds__(256) ksmac_thin_kernel(KsMacArgs a, int units)
     for (int u = 0; u < CPT; u++) {
       const int z = z0 + u < units ? z0 + u : units - 1;  // clamp: the tail's extra work is discarded
       const u64* C0 = a.C0 + (size_t)z * LN;
-      const u64* D = a.D + (size_t)z * (LT > 0 ? LT : a.L) * LN;
+      const u64* D = a.D + (size_t)z * (LT > 0 ? LT : a.ND) * LN;
       c0v[u] = __ldg(C0 + (size_t)l * N + jp);
       if constexpr (LT > 0) {
         if (key == nullptr) {
@@ -887,12 +949,12 @@ __global__ void __launch_bounds__(256) ksmac_thin_kernel(KsMacArgs a, int units)
         }
       } else {
         const u64* C0 = a.C0 + (size_t)z * LN;
-        const u64* D = a.D + (size_t)z * a.L * LN;
+        const u64* D = a.D + (size_t)z * a.ND * LN;
         if (key == nullptr) {
           r0 = c0v[u];
-          r1 = __ldg(D + ((size_t)l * a.L + l) * N + j);
+          r1 = ident_c1(D, a.L, a.ND, a.wd, N, l, j, cst.q);
         } else {
-          ks_pair_any(D, C0, key, a.L, a.logN, l, j, jp, cst, r0, r1);
+          ks_pair_any(D, C0, key, a.L, a.logN, l, j, jp, cst, r0, r1, a.ND);
         }
       }
       const double x0h = (double)(uint32_t)(r0 >> 30), x0l = (double)(uint32_t)(r0 & M30);
@@ -934,12 +996,13 @@ __global__ void __launch_bounds__(256) permauto_kernel(KsMacArgs a, u64* __restr
   const size_t LN = (size_t)L * N;
   const u64* key = a.keys[t];
   u64* out = R + ((size_t)z * a.K + (size_t)t * a.Jcb) * 2 * LN + (size_t)l * N + j;
+  const int ND = LT > 0 ? LT : a.ND;
   const u64* C0b = a.C0 + (size_t)z * a.Jcb * LN;
-  const u64* Db = a.D + (size_t)z * a.Jcb * L * LN;
+  const u64* Db = a.D + (size_t)z * a.Jcb * ND * LN;
   if (key == nullptr) {  // identity tap: R = (C0, D_{l,l})
     for (int c = 0; c < a.Jcb; c++) {
       const u64 r0 = __ldg(C0b + (size_t)c * LN + (size_t)l * N + j);
-      const u64 r1 = __ldg(Db + (size_t)c * L * LN + ((size_t)l * L + l) * N + j);
+      const u64 r1 = ident_c1(Db + (size_t)c * ND * LN, L, ND, a.wd, N, l, j, cst.q);
       __stcs(out + (size_t)c * 2 * LN, r0);
       __stcs(out + (size_t)c * 2 * LN + LN, r1);
     }
@@ -980,7 +1043,7 @@ __global__ void __launch_bounds__(256) permauto_kernel(KsMacArgs a, u64* __restr
   } else {
     for (int c = 0; c < a.Jcb; c++) {
       u64 r0, r1;
-      ks_pair_any(Db + (size_t)c * L * LN, C0b + (size_t)c * LN, key, L, a.logN, l, j, jp, cst, r0, r1);
+      ks_pair_any(Db + (size_t)c * ND * LN, C0b + (size_t)c * LN, key, L, a.logN, l, j, jp, cst, r0, r1, ND);
       __stcs(out + (size_t)c * 2 * LN, r0);
       __stcs(out + (size_t)c * 2 * LN + LN, r1);
     }
@@ -1988,7 +2051,8 @@ struct MaskArgs {
   int L, logN;
   size_t n;
   const uint32_t* c1;   // per poly-group o: counter word 1 (encryption index or Galois element)
-  uint32_t c2_mul;      // key masks: group o = (element, digit i): c2 = 256 i + l; encryption: c2 = l
+  uint32_t digits;      // key masks: group o = (element, digit dd) with `digits` digits: c2 = 256 dd + l;
+                        // encryption (0): c2 = l
   QArr qa;
 };
 __global__ void gen_mask_kernel(MaskArgs m, u64* __restrict__ out) {
@@ -2000,9 +2064,9 @@ __global__ void gen_mask_kernel(MaskArgs m, u64* __restrict__ out) {
     const int l = (int)(ol % m.L);
     const size_t o = ol / m.L;
     uint32_t c1, c2;
-    if (m.c2_mul) {  // key: o = element index * L + digit
-      c1 = m.c1[o / m.L];
-      c2 = 256u * (uint32_t)(o % m.L) + (uint32_t)l;
+    if (m.digits) {  // key: o = element index * digits + digit
+      c1 = m.c1[o / m.digits];
+      c2 = 256u * (uint32_t)(o % m.digits) + (uint32_t)l;
     } else {
       c1 = m.c1[o];
       c2 = (uint32_t)l;
@@ -2026,7 +2090,7 @@ __global__ void gen_error_kernel(u64 seed, uint32_t purpose, int logN, size_t n,
 
 // c = INTT(NTT(a) .* NTT(s)) and the client's combination, per (poly o, limb):
 //   encryption: c0 = [Delta m + a s + e], c1 = [-a]           (symmetric BFV)
-//   key digit i: b = [-a s + e_i + [i == l] s(X^g)], a kept  (reading R5, RNS-digit gadget)
+//   key digit dd = i V + v: b = [-a s + e_dd + [i == l] 2^{w v} s(X^g)], a kept  (reading R5; sub-digit base)
 struct ClientInvJob {
   const u64* An;        // [n][L][N] NTT(a)
   const u64* Sn;        // [L][N] NTT(s), then [L][N] Shoup companions
@@ -2035,8 +2099,9 @@ struct ClientInvJob {
   const u64* M;         // encryption: [n][N] plaintext coefficients (< t); keys: null
   const u64* Sg;        // keys: [n_elts][L][N] s(X^g) lifted per limb; encryption: null
   u64* out;             // [n][2][L][N]
-  int L, N, digits;     // digits = L for keys (o = element * L + i), 0 for encryption
+  int L, N, digits;     // digits = ND for keys (o = element * ND + dd), 0 for encryption
   QArr qa, delta;       // delta: Delta mod q_l
+  int V, wd;            // sub-digits per limb and base bits (V = 1: one digit per limb)
   int limb, o;
   __device__ void bind(int b) {
     o = b / L;
@@ -2058,9 +2123,12 @@ struct ClientInvJob {
       c[(size_t)limb * N + k] = csub(csub(csub(dm + as, q) + er, q), q);
       c[(size_t)(L + limb) * N + k] = A[at] ? q - A[at] : 0;
     } else {
-      const int i = o % digits;
+      const int dd = o % digits;
       u64 b = csub((as ? q - as : 0) + er, q);
-      if (i == limb) b = csub(b + Sg[((size_t)(o / digits) * L + limb) * N + k], q);
+      if (dd / V == limb) {
+        const u64 sgv = Sg[((size_t)(o / digits) * L + limb) * N + k];
+        b = csub(b + (V > 1 ? mulmod_slow(sgv, (1ull << (wd * (dd % V))) % q, q) : sgv), q);
+      }
       c[(size_t)limb * N + k] = b;
       c[(size_t)(L + limb) * N + k] = A[at];
     }
@@ -2119,7 +2187,7 @@ hy_status shoup_table(const hy_params* p, const u64* w, u64* wsh, size_t npoly, 
 hy_status key_to_ntt(const hy_params* p, const u64* key_coeff, u64* key_ntt, cudaStream_t s) {
   // key [L][2][L][N] -> NTT per (digit, comp, limb); Shoup companions in the following block, then
   // the 30-bit split values (the exact-product MAC producers, ksmac_v3)
-  const size_t npoly = 2 * p->L;  // groups of L limbs
+  const size_t npoly = 2 * p->ND;  // groups of L limbs
   const size_t words = npoly * p->L * p->N;
   HY_TRY(ntt_poly_fwd(p, key_coeff, key_ntt, npoly, s));
   HY_TRY(shoup_table(p, key_ntt, key_ntt + words, npoly, s));
@@ -2131,7 +2199,10 @@ hy_status key_to_ntt(const hy_params* p, const u64* key_coeff, u64* key_ntt, cud
 
 hy_status permdecomp(const hy_params* p, const u64* ct, size_t nct, u64* D, u64* C0, cudaStream_t s) {
   PermDecompJob j{ct, D, C0, (int)p->L, (int)p->N, qarr(p)};
-  return launch_fwd(p, j, nct * (p->L * p->L + p->L), s);
+  j.ND = (int)p->ND;
+  j.V = (int)p->V;
+  j.wd = (int)p->w_dcmp;
+  return launch_fwd(p, j, nct * (p->ND * p->L + p->L), s);
 }
 
 // MAC-kernel timing (bench): record an event before/after each MAC launch when enabled
@@ -2181,14 +2252,17 @@ hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
   a.kscale = (int)lay.k;
   a.cn = (int)lay.cn;
   a.lcs = limb_consts(p);
+  a.ND = (int)p->ND;
+  a.wd = (int)p->w_dcmp;
   const int units = (int)(dw ? nunits * lay.Jc : nunits);
   const int tile = hy_mac_tile(w->M, dw);
   const int path = w->mac_path;
+  const int Lsel = p->ND == p->L ? (int)p->L : 0;  // a sub-digit base takes the generic kernels
   if (path == HY_MAC_THIN || path == HY_MAC_FP64_FUSED) {  // key switching fused into the FP64 MAC
     HY_TRY(mac_mark(w, s));
     if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[0], s));
     hy_status st;
-    switch (p->L) {  // compile-time digit count for the common L
+    switch (Lsel) {  // compile-time digit count for the common L
       case 2: st = launch_ksmac<2>(a, tile, units, s); break;
       case 3: st = launch_ksmac<3>(a, tile, units, s); break;
       case 5: st = launch_ksmac<5>(a, tile, units, s); break;
@@ -2213,14 +2287,14 @@ hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
   const bool fp64_mac = path == HY_MAC_FP64_SPLIT;
   // dense: PermAuto materialises R for a batch of units, the MAC GEMM consumes it
   const size_t LN = (size_t)p->L * p->N;
-  const int mrows = lay.cn == 2 ? w->M / 2 : w->M;  // output ciphertexts per unit
+  const int mrows = lay.cn == 4 ? w->M / 4 : lay.cn == 2 ? w->M / 2 : w->M;  // output P rows per unit
   for (int u0 = 0; u0 < units; u0 += w->r_units) {
     const int nb = std::min(w->r_units, units - u0);
     KsMacArgs b = a;
-    b.D = a.D + (size_t)u0 * a.Jcb * p->L * LN;
+    b.D = a.D + (size_t)u0 * a.Jcb * p->ND * LN;
     b.C0 = a.C0 + (size_t)u0 * a.Jcb * LN;
     b.out = a.out + (size_t)u0 * mrows * 2 * LN;
-    switch (p->L) {
+    switch (Lsel) {
       case 2: HY_TRY(launch_permauto<2>(b, w->d_R, nb, s)); break;
       case 3: HY_TRY(launch_permauto<3>(b, w->d_R, nb, s)); break;
       case 5: HY_TRY(launch_permauto<5>(b, w->d_R, nb, s)); break;
@@ -2329,12 +2403,16 @@ hy_status finish_coef2(const hy_weights* w, size_t nunits, u64* ct_out, cudaStre
                         limb_consts(p), sv, svsh));
   HY_LAUNCH_CHECK();
   PermDecompJob jd{w->d_P + ctw, w->d_D, w->d_C0, (int)L, (int)N, qarr(p), 2 * ctw};  // P_1 of every output
-  HY_TRY(launch_fwd(p, jd, nout * (L * L + L), s));
+  jd.ND = (int)p->ND;
+  jd.V = (int)p->V;
+  jd.wd = (int)p->w_dcmp;
+  HY_TRY(launch_fwd(p, jd, nout * (p->ND * L + L), s));
   KsApplyArgs ka;
+  ka.ND = (int)p->ND;
   ka.c0 = w->d_C0;
   ka.c0_stride = L * N;
   ka.D = w->d_D;
-  ka.D_stride = L * L * N;
+  ka.D_stride = p->ND * L * N;
   ka.diag = nullptr;
   ka.diag_stride = 0;
   ka.add = nullptr;
@@ -2351,6 +2429,47 @@ hy_status finish_coef2(const hy_weights* w, size_t nunits, u64* ct_out, cudaStre
   return launch_inv(p, jx, nout * 2 * L, s);
 }
 
+// HRot of the partial sums P_d (NTT form) of every output by the Galois element with key `key` /
+// action `act`, added to `add` (hoisted HRot of PAPER.md:373-378 applied to one ct): digits of
+// P_d.c1 need coefficient form (INTT), then NTT into every limb (with one digit per limb, digit i in
+// limb i is P_d.c1 limb i itself)
+static hy_status rotate_partials(const hy_weights* w, size_t nout, const u64* Pd, size_t pstride, const u64* add,
+                                 size_t add_stride, const u64* key, GaloisAct act, cudaStream_t s) {
+  const hy_params* p = w->p;
+  const size_t L = p->L, N = p->N, ND = p->ND;
+  const bool sub = ND != L;
+  u64* dig = w->d_D2 + nout * ND * L * N;  // [o][L][N] scratch after the digit NTTs
+  StridedInvJob ja{Pd + L * N, pstride, dig, (int)L, (int)N};
+  HY_TRY(launch_inv(p, ja, nout * L, s));
+  DigitLiftJob jb{dig, w->d_D2, (int)L, (int)N, qarr(p)};
+  if (sub) {
+    jb.ND = (int)ND;
+    jb.V = (int)p->V;
+    jb.wd = (int)p->w_dcmp;
+    HY_TRY(launch_fwd(p, jb, nout * ND * L, s));
+  } else if (L > 1) {
+    HY_TRY(launch_fwd(p, jb, nout * L * (L - 1), s));
+  }
+  KsApplyArgs ka;
+  ka.ND = (int)ND;
+  ka.c0 = Pd;
+  ka.c0_stride = pstride;
+  ka.D = w->d_D2;
+  ka.D_stride = ND * L * N;
+  ka.diag = sub ? nullptr : Pd + L * N;
+  ka.diag_stride = pstride;
+  ka.add = add;
+  ka.add_stride = add_stride;
+  ka.key = key;
+  ka.act = act;
+  ka.out = w->d_X;
+  ka.L = (int)L;
+  ka.logN = (int)p->logN;
+  ka.total = nout * L * N;
+  ka.lcs = limb_consts(p);
+  return launch_ks_apply(ka, s);
+}
+
 hy_status finish_outputs(const hy_weights* w, size_t nunits, u64* ct_out, cudaStream_t s) {
   const hy_params* p = w->p;
   const hy_layout& lay = w->lay;
@@ -2359,31 +2478,18 @@ hy_status finish_outputs(const hy_weights* w, size_t nunits, u64* ct_out, cudaSt
   const size_t ct_words = 2 * L * N;
   if (lay.cn == 2 && !w->shape.depthwise) {
     // S4 alignment: Out_g = P_{g,0} + RowSwap(P_{g,1}); RowSwap = hoisted HRot
-    // with g = 2N-1: digits of P_{g,1}.c1 need coefficient form (INTT), then NTT in other limbs.
-    u64* dig = w->d_D2 + nout * L * L * N;  // [o][L][N] scratch after D2
-    StridedInvJob ja{w->d_P + ct_words + L * N, 2 * ct_words, dig, (int)L, (int)N};
-    HY_TRY(launch_inv(p, ja, nout * L, s));
-    if (L > 1) {
-      DigitLiftJob jb{dig, w->d_D2, (int)L, (int)N, qarr(p)};
-      HY_TRY(launch_fwd(p, jb, nout * L * (L - 1), s));
-    }
-    KsApplyArgs ka;
-    ka.c0 = w->d_P + ct_words;  // P_{g,1}.c0
-    ka.c0_stride = 2 * ct_words;
-    ka.D = w->d_D2;
-    ka.D_stride = L * L * N;
-    ka.diag = w->d_P + ct_words + L * N;  // P_{g,1}.c1: digit i in limb i is already NTT(d_i)
-    ka.diag_stride = 2 * ct_words;
-    ka.add = w->d_P;  // P_{g,0}
-    ka.add_stride = 2 * ct_words;
-    ka.key = w->d_swap_key;
-    ka.act = GaloisAct{0u, 1u};  // X -> X^{2N-1}: exchange the two slot rows
-    ka.out = w->d_X;
-    ka.L = (int)L;
-    ka.logN = (int)p->logN;
-    ka.total = nout * L * N;
-    ka.lcs = limb_consts(p);
-    HY_TRY(launch_ks_apply(ka, s));
+    // with g = 2N-1 (exchange of the two slot rows)
+    HY_TRY(rotate_partials(w, nout, w->d_P + ct_words, 2 * ct_words, w->d_P, 2 * ct_words, w->d_swap_key,
+                           GaloisAct{0u, 1u}, s));
+    OutInvJob jx{w->d_X, ct_words, ct_out, (int)L, (int)N};
+    return launch_inv(p, jx, nout * 2 * L, s);
+  }
+  if (lay.cn == 4) {
+    // c_n = 4 alignment: Out_g = P_{g,0} + sum_{d=1..3} HRot_{g_d}(P_{g,d}), g_d moving slot group c
+    // to c xor d (row swap x half-row rotation; oracle conv.align_elts)
+    for (int d = 1; d < 4; d++)
+      HY_TRY(rotate_partials(w, nout, w->d_P + d * ct_words, 4 * ct_words, d == 1 ? w->d_P : w->d_X,
+                             d == 1 ? 4 * ct_words : ct_words, w->d_align_key[d - 1], w->h_align_act[d - 1], s));
     OutInvJob jx{w->d_X, ct_words, ct_out, (int)L, (int)N};
     return launch_inv(p, jx, nout * 2 * L, s);
   }
@@ -2393,16 +2499,17 @@ hy_status finish_outputs(const hy_weights* w, size_t nunits, u64* ct_out, cudaSt
 
 hy_status rotate_ct(const hy_params* p, const u64* ct_in, GaloisAct act, const u64* key, u64* ct_out, size_t n,
                     u64* work, cudaStream_t s) {
-  const size_t L = p->L, N = p->N;
+  const size_t L = p->L, N = p->N, ND = p->ND;
   u64* D = work;
-  u64* C0 = work + n * L * L * N;
+  u64* C0 = work + n * ND * L * N;
   HY_TRY(permdecomp(p, ct_in, n, D, C0, s));
-  u64* X = work + n * (L * L + L) * N;  // [n][2][L][N]
+  u64* X = work + n * (ND * L + L) * N;  // [n][2][L][N]
   KsApplyArgs ka;
+  ka.ND = (int)ND;
   ka.c0 = C0;
   ka.c0_stride = L * N;
   ka.D = D;
-  ka.D_stride = L * L * N;
+  ka.D_stride = ND * L * N;
   ka.diag = nullptr;
   ka.diag_stride = 0;
   ka.add = nullptr;
@@ -2443,7 +2550,7 @@ hy_status client_encrypt(const hy_params* p, u64 seed, const u64* s_ntt, const u
   HY_TRY(ntt_poly_fwd(p, A, An, n, st));
   QArr dl;
   for (size_t l = 0; l < L; l++) dl.q[l] = delta_l[l];
-  ClientInvJob j{An, s_ntt, A, E, m_dev, nullptr, ct_out, (int)L, (int)N, 0, qarr(p), dl};
+  ClientInvJob j{An, s_ntt, A, E, m_dev, nullptr, ct_out, (int)L, (int)N, 0, qarr(p), dl, 1, 0};
   return launch_inv(p, j, n * L, st);
 }
 
@@ -2451,21 +2558,22 @@ hy_status client_encrypt(const hy_params* p, u64 seed, const u64* s_ntt, const u
 // keys_out [n][L digits][2][L limbs][N] coefficient form
 hy_status client_keygen(const hy_params* p, u64 seed, const u64* s_ntt, const int8_t* sk8_dev, const uint32_t* elts_dev,
                         size_t n_elts, u64* keys_out, u64* work, cudaStream_t st) {
-  const size_t L = p->L, N = p->N, n = n_elts * L;  // polys groups o = element * L + digit
+  const size_t L = p->L, N = p->N, ND = p->ND, n = n_elts * ND;  // poly groups o = element * ND + digit
   u64* A = work;                          // [n][L][N]
   u64* An = A + n * L * N;
   u64* Sg = An + n * L * N;               // [n_elts][L][N]
   int32_t* E = reinterpret_cast<int32_t*>(Sg + n_elts * L * N);  // [n][N]
-  MaskArgs ma{seed, 4u, (int)L, (int)p->logN, n, elts_dev, 1u, qarr(p)};
+  MaskArgs ma{seed, 4u, (int)L, (int)p->logN, n, elts_dev, (uint32_t)ND, qarr(p)};
   gen_mask_kernel<<<148 * 8, 256, 0, st>>>(ma, A);
   HY_LAUNCH_CHECK();
-  gen_error_kernel<<<148 * 8, 256, 0, st>>>(seed, 5u, (int)p->logN, n, elts_dev, (int)L, E);
+  gen_error_kernel<<<148 * 8, 256, 0, st>>>(seed, 5u, (int)p->logN, n, elts_dev, (int)ND, E);
   HY_LAUNCH_CHECK();
   automorph_secret_kernel<<<148 * 4, 256, 0, st>>>(sk8_dev, elts_dev, (int)n_elts, (int)L, (int)p->logN, qarr(p), Sg);
   HY_LAUNCH_CHECK();
   HY_TRY(ntt_poly_fwd(p, A, An, n, st));
   QArr dl{};
-  ClientInvJob j{An, s_ntt, A, E, nullptr, Sg, keys_out, (int)L, (int)N, (int)L, qarr(p), dl};
+  ClientInvJob j{An, s_ntt, A, E, nullptr, Sg, keys_out, (int)L, (int)N, (int)ND, qarr(p), dl, (int)p->V,
+                 (int)p->w_dcmp};
   return launch_inv(p, j, n * L, st);
 }
 
@@ -2479,15 +2587,16 @@ hy_status decrypt_phase(const hy_params* p, const u64* s_ntt, const u64* s_ntt_s
 
 }  // namespace hyk
 
-int hy_mac_path(int M, int L, bool depthwise, bool coef_ok) {
+int hy_mac_path(int M, int L, bool depthwise, bool coef_ok, int cn, bool subdigits) {
   if (depthwise) return HY_MAC_THIN;
+  if (cn == 4) return M <= 32 ? HY_MAC_FP64_FUSED : HY_MAC_FP64_SPLIT;  // WHT-4 epilogue: FP64 MAC only
   static const bool fp64 = getenv("HY_MAC_FP64") != nullptr;    // A/B switches
   static const bool split = getenv("HY_SPLIT_TC") != nullptr;
   if (coef_ok && !fp64 && !split) return HY_MAC_TC_COEF;
   if (fp64) return M <= 32 ? HY_MAC_FP64_FUSED : HY_MAC_FP64_SPLIT;
   // M <= 32 (latency-bound small layers, e.g. C1/C2): the FP64 fused kernel is faster (measured,
-  // DESIGN.md §4); 32 < M <= 128: key switching fused into the tcgen05 MAC
+  // DESIGN.md §4); 32 < M <= 128: key switching fused into the tcgen05 MAC (one digit per limb only)
   if (!split && M <= 32) return HY_MAC_FP64_FUSED;
-  if (!split && M <= 128 && (L == 2 || L == 3 || L == 5)) return HY_MAC_TC_FUSED;
+  if (!split && !subdigits && M <= 128 && (L == 2 || L == 3 || L == 5)) return HY_MAC_TC_FUSED;
   return HY_MAC_TC_SPLIT;
 }

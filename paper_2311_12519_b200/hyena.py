@@ -17,18 +17,19 @@ __all__ = ["HyenaError", "hy_conv_shape", "hy_layout", "load_library", "library_
            "hy_weights_layout", "hy_weights_destroy", "hy_conv_eval", "hy_conv_eval_host", "hy_poly_mul",
            "hy_ntt_roundtrip", "hy_rotate", "hy_decrypt_debug", "hy_kernel_launches", "hy_weights_set_stage_events",
            "hy_weights_mac_time", "hy_weights_mac_path", "hy_weights_set_mac_path", "hy_secret_key", "hy_keygen",
-           "hy_encrypt", "MAC_PATHS", "layout_dict", "EXPORTED"]
+           "hy_encrypt", "hy_layout_accounting", "hy_accounting", "MAC_PATHS", "layout_dict", "EXPORTED"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 HY_MAX_TAPS = 49
 HY_MAX_GALOIS = 64
 
 # every symbol include/hyena.h declares
-EXPORTED = ["hy_last_error", "hy_plan_layout", "hy_params_create", "hy_params_destroy", "hy_keys_upload",
+EXPORTED = ["hy_last_error", "hy_plan_layout", "hy_params_create", "hy_params_create2", "hy_params_destroy",
+            "hy_keys_upload",
             "hy_encode_weights", "hy_weights_layout", "hy_weights_destroy", "hy_conv_eval", "hy_conv_eval_host",
             "hy_poly_mul", "hy_ntt_roundtrip", "hy_rotate", "hy_decrypt_debug", "hy_kernel_launches",
             "hy_weights_set_stage_events", "hy_weights_mac_time", "hy_weights_mac_path", "hy_weights_set_mac_path",
-            "hy_secret_key", "hy_keygen", "hy_encrypt"]
+            "hy_secret_key", "hy_keygen", "hy_encrypt", "hy_layout_accounting"]
 
 # S2 + S3 kernel choices (include/hyena.h hy_weights_mac_path)
 MAC_PATHS = {"thin": 0, "tc_fused": 1, "tc_split": 2, "fp64_fused": 3, "fp64_split": 4, "tc_coef": 5}
@@ -51,6 +52,13 @@ class hy_layout(ctypes.Structure):
                 + [(n, ctypes.c_uint32) for n in ("k", "scale", "h")]
                 + [("sign_coeff", ctypes.c_int32), ("n_galois", ctypes.c_uint32),
                    ("galois", ctypes.c_uint32 * HY_MAX_GALOIS)])
+
+
+class hy_accounting(ctypes.Structure):
+    _fields_ = ([(n, ctypes.c_uint64) for n in ("input_ct_bytes", "output_ct_bytes", "input_ct_bytes_paper",
+                                                 "model_bytes_paper", "model_bytes_conventional",
+                                                 "model_bytes_device", "key_bytes")]
+                + [("n_keys", ctypes.c_uint32), ("rotations", ctypes.c_uint32), ("coef_macs", ctypes.c_uint64)])
 
 
 def layout_dict(lay: hy_layout) -> dict:
@@ -81,6 +89,7 @@ def load_library() -> ctypes.CDLL:
         "hy_last_error": (ctypes.c_char_p, []),
         "hy_plan_layout": (i32, [u32, u64, ctypes.POINTER(hy_conv_shape), ctypes.POINTER(hy_layout)]),
         "hy_params_create": (i32, [u32, vp, u32, u64, ctypes.c_int, ctypes.POINTER(vp)]),
+        "hy_params_create2": (i32, [u32, vp, u32, u64, u32, ctypes.c_int, ctypes.POINTER(vp)]),
         "hy_params_destroy": (None, [vp]),
         "hy_keys_upload": (i32, [vp, u32, vp, vp, ctypes.c_int]),
         "hy_encode_weights": (i32, [vp, ctypes.POINTER(hy_conv_shape), vp, ctypes.POINTER(vp)]),
@@ -98,6 +107,8 @@ def load_library() -> ctypes.CDLL:
         "hy_weights_mac_path": (i32, [vp, ctypes.POINTER(i32)]),
         "hy_weights_set_mac_path": (i32, [vp, i32]),
         "hy_secret_key": (i32, [vp, u64, vp]),
+        "hy_layout_accounting": (i32, [ctypes.POINTER(hy_layout), ctypes.POINTER(hy_conv_shape), u32, u32,
+                                       ctypes.POINTER(hy_accounting)]),
         "hy_keygen": (i32, [vp, u64, u32, vp, vp, ctypes.c_int]),
         "hy_encrypt": (i32, [vp, u64, vp, sz, u32, vp, vp]),
     }
@@ -151,10 +162,12 @@ def hy_plan_layout(N: int, t: int, **shape) -> hy_layout:
     return lay
 
 
-def hy_params_create(N: int, primes: Sequence[int], t: int, device: int = 0) -> int:
+def hy_params_create(N: int, primes: Sequence[int], t: int, device: int = 0, w_dcmp: int = 0) -> int:
+    """w_dcmp > 0: decomposition base 2^w_dcmp inside each limb (hy_params_create2)."""
     q = (ctypes.c_uint64 * len(primes))(*[int(x) for x in primes])
     out = ctypes.c_void_p()
-    _check(load_library().hy_params_create(N, q, len(primes), t, device, ctypes.byref(out)), "hy_params_create")
+    _check(load_library().hy_params_create2(N, q, len(primes), t, w_dcmp, device, ctypes.byref(out)),
+           "hy_params_create2")
     return out.value
 
 
@@ -296,3 +309,12 @@ def hy_encrypt(p: int, seed: int, m: np.ndarray, ct_out, first: int = 0, stream=
     mm = np.ascontiguousarray(m, dtype=np.uint64)
     _check(load_library().hy_encrypt(p, seed, mm.ctypes.data, mm.shape[0], first, _dev_ptr(ct_out),
                                      _stream(stream)), "hy_encrypt")
+
+
+def hy_layout_accounting(lay: hy_layout, L: int, ND: int = 0, **shape) -> dict:
+    """Storage / communication accounting of a planned layout (host only; include/hyena.h)."""
+    out = hy_accounting()
+    s = _shape(**shape)
+    _check(load_library().hy_layout_accounting(ctypes.byref(lay), ctypes.byref(s), L, ND or L, ctypes.byref(out)),
+           "hy_layout_accounting")
+    return {n: getattr(out, n) for n, _ in hy_accounting._fields_}

@@ -13,8 +13,9 @@ multipliers 0xD2511F53 / 0xCD9E8D57, Weyl key increments 0x9E3779B9 / 0xBB67AE85
 Counter assignment (one Philox block per coefficient k):
   secret s[k]                       ctr = (k, 0, 0, 1)
   encryption j: mask a_l[k]         ctr = (k, j, l, 2)        error e[k]   ctr = (k, j, 0, 3)
-  key for Galois element g, digit i: mask a_{i,l}[k]  ctr = (k, g, 256 i + l, 4)
-                                     error e_i[k]      ctr = (k, g, 256 i, 5)
+  key for Galois element g, gadget digit dd (dd = i for one digit per limb, i V + v with a
+  sub-digit base):                   mask a_{dd,l}[k]  ctr = (k, g, 256 dd + l, 4)
+                                     error e_dd[k]     ctr = (k, g, 256 dd, 5)
 Mappings of the block (x0, x1, x2, x3) (32-bit words):
   uniform residue mod q:  floor(X q / 2^128), X = x3 2^96 + x2 2^64 + x1 2^32 + x0  (exact, bias < 2^-64)
   ternary:                floor(Y 3 / 2^64) - 1,  Y = x1 2^32 + x0
@@ -112,14 +113,14 @@ def enc_error(seed: int, j: int, N: int) -> np.ndarray:
     return cbd20(philox4x32(k, j, 0, P_ENC_E, seed))
 
 
-def key_mask(seed: int, g: int, primes: Sequence[int], N: int) -> np.ndarray:
-    """uint64 [L digits][L limbs][N] (masks a_i of the key for Galois element g)."""
+def key_mask(seed: int, g: int, primes: Sequence[int], N: int, ND: int = 0) -> np.ndarray:
+    """uint64 [ND digits][L limbs][N] (masks a_dd of the key for Galois element g; ND = L default)."""
     k = np.arange(N, dtype=np.uint64)
-    L = len(primes)
+    ND = ND or len(primes)
     return np.stack([np.stack([uniform_mod(philox4x32(k, g, 256 * i + l, P_KEY_A, seed), q)
-                               for l, q in enumerate(primes)]) for i in range(L)])
+                               for l, q in enumerate(primes)]) for i in range(ND)])
 
 
-def key_error(seed: int, g: int, L: int, N: int) -> np.ndarray:
+def key_error(seed: int, g: int, ND: int, N: int) -> np.ndarray:
     k = np.arange(N, dtype=np.uint64)
-    return np.stack([cbd20(philox4x32(k, g, 256 * i, P_KEY_E, seed)) for i in range(L)])
+    return np.stack([cbd20(philox4x32(k, g, 256 * i, P_KEY_E, seed)) for i in range(ND)])

@@ -94,3 +94,37 @@ def test_params_create_validation_without_gpu(hy):
         hy.hy_params_create(4096, [2147483647], 65537)            # 2^31-1: prime, not 1 mod 8192
     with pytest.raises(hy.HyenaError, match=r"\(2\^20, 2\^60\)"):
         hy.hy_params_create(4096, [2305843009213693951], 65537)   # 2^61-1: prime but too large
+
+
+def test_layout_accounting_matches_paper_tables(hy):
+    """hy_layout_accounting (host only) reproduces PAPER.md Table 2's input-ct and model columns and
+    the :561-562 storage example with one 60-bit prime (the paper's setting, L = 1), and agrees with
+    the oracle's cost model; the library's own layout counts its J / Jout ciphertexts."""
+    import json
+    from oracle import costmodel
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "paper_values.json")))
+    MB = 1 << 20
+    for r in gold["table2_rows"]["rows"]:
+        H, n = r["H"], r["n"]
+        t = 65537
+        shape = dict(Ci=r["Ci"], Co=r["Co"], H=H - 2, W=H - 2, kh=3, kw=3, pad=1, batch=1, force_cn=1)
+        lay = hy.hy_plan_layout(n, t, **shape)
+        acc = hy.hy_layout_accounting(lay, 1, **shape)
+        assert acc["input_ct_bytes_paper"] == costmodel.input_ct_bytes(r["Ci"], H, n)
+        assert round(acc["input_ct_bytes_paper"] / MB) == r["input_ct_MB"]
+        assert acc["model_bytes_paper"] == costmodel.model_bytes_proposed(r["Ci"], r["Co"], 3)
+        assert abs(acc["model_bytes_paper"] / MB - r["model_MB"]) <= 0.01 * r["model_MB"] + 0.005
+    # PAPER.md:561-562: a 2 x 3 x 3 kernel at n = 2048, c_n = 2: 16.1 KB vs 288 KB
+    shape = dict(Ci=2, Co=1, H=8, W=8, kh=3, kw=3, pad=1, batch=1, force_cn=2)
+    lay = hy.hy_plan_layout(2048, 65537, **shape)
+    acc = hy.hy_layout_accounting(lay, 1, **shape)
+    assert acc["model_bytes_paper"] == costmodel.storage_proposed_bytes(18, 2048) == 16528
+    assert acc["model_bytes_conventional"] == costmodel.storage_conventional_bytes(18, 2048) == 288 * 1024
+    # C4 with this library's layout: bands of 14 valid rows -> 4096 input and output cts
+    import synth
+    cfg = synth.configs()["C4"]
+    lay = hy.hy_plan_layout(cfg.N, cfg.t, **cfg.shape_dict())
+    acc = hy.hy_layout_accounting(lay, 3, **cfg.shape_dict())
+    assert acc["input_ct_bytes"] == acc["output_ct_bytes"] == 4096 * 2 * 3 * 8192 * 8
+    assert acc["rotations"] == 4096 * 8 and acc["n_keys"] == 8
+    assert acc["coef_macs"] == 64 * 64 * 576 * 2 * 3 * 8192

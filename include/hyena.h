@@ -110,6 +110,19 @@ typedef struct {
 hy_status hy_layout_accounting(const hy_layout* lay, const hy_conv_shape* shape, uint32_t L, uint32_t ND,
                                hy_accounting* out);
 
+/* Noise-driven decomposition-base selection (SURVEY §8(f) NEXT-4; PAPER.md:587-617, :1470 [app]).
+ * hy_noise_estimate: host-only heuristic estimate of log2 ||v||_inf of one layer's output noise for a
+ *   key-switching base 2^w_dcmp (0: one digit per limb) and weights |w| <= w_max, and the budget
+ *   log2(Delta / 2); model in api.cu (one HRot, lazy MAC, c_n = 2 [k, -k] / c_n = 4 dense PMults,
+ *   alignment), calibrated against the oracle's noise meter.
+ * hy_select_dcmp_base: the base with the FEWEST digits (largest base) whose estimate leaves
+ *   margin_bits below the budget: w_dcmp = 0 when one digit per limb suffices.
+ * Errors: HY_EINVAL (bad shape, no base meets the margin). */
+hy_status hy_noise_estimate(uint32_t N, const uint64_t* q_primes, uint32_t L, uint64_t t, const hy_conv_shape* shape,
+                            uint32_t w_max, uint32_t w_dcmp, double* log2_noise, double* log2_budget);
+hy_status hy_select_dcmp_base(uint32_t N, const uint64_t* q_primes, uint32_t L, uint64_t t,
+                              const hy_conv_shape* shape, uint32_t w_max, double margin_bits, uint32_t* w_dcmp);
+
 /* Thread-local message describing the last failing call ("" if none). */
 const char* hy_last_error(void);
 

@@ -6,6 +6,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "hy_common.cuh"
@@ -304,6 +305,76 @@ extern "C" hy_status hy_layout_accounting(const hy_layout* lay, const hy_conv_sh
   a.coef_macs = (dw ? (u64)lay->U * lay->Jc : lay->U) * M * K * 2 * L * N;
   *out = a;
   return HY_OK;
+}
+
+// Noise-driven decomposition-base selection (the smaller the
+// noise growth of the convolution, the larger the key-switching decomposition base that still
+// decrypts, and the fewer digits every HRot costs).  Heuristic infinity-norm model (6 sigma tails,
+// independent random-walk growth), calibrated against the oracle's noise meter
+// (tests/test_abi.py::test_noise_model_tracks_the_oracle):
+//   one rotation:  sigma_rot = sqrt(ND N / 3) B_d sigma_e   (ND digits < B_d = 2^w or q, CBD sigma_e = sqrt(10))
+//   lazy MAC:      sigma_mac = sqrt(K) (w_max / sqrt 3) sigma_rot
+//   c_n = 1:       sigma_out = sigma_mac
+//   c_n = 2:       sigma_out = sqrt 2 max(k, 2 |[k h]_t|) sigma_mac + sigma_rot      ([k, -k] PMult, row swap)
+//   c_n = 4:       sigma_out = 2 sqrt 3 sqrt N (t / sqrt 12) sigma_mac + sqrt 3 sigma_rot (dense rows)
+//   noise = log2(6 sigma_out),  budget = log2(Delta / 2) ~= log2(Q / t) - 1.
+static hy_status noise_model(uint32_t N, const uint64_t* q, uint32_t L, uint64_t t, const hy_conv_shape* sh,
+                             uint32_t w_max, uint32_t w, double* noise, double* budget) {
+  hy_layout lay;
+  HY_TRY(hy_plan_layout(N, t, sh, &lay));
+  double qbits = 0, logQ = 0;
+  for (uint32_t l = 0; l < L; l++) {
+    uint32_t b = 0;
+    while (b < 64 && (q[l] >> b)) b++;
+    qbits = std::max(qbits, (double)b);
+    logQ += std::log2((double)q[l]);
+  }
+  const double V = w ? std::ceil(qbits / w) : 1.0, ND = L * V;
+  const double Bd = std::exp2(w ? (double)w : qbits), sig = std::sqrt(10.0);
+  const double s_rot = std::sqrt(ND * N / 3.0) * Bd * sig;
+  const double K = sh->depthwise ? (double)lay.n_taps : (double)lay.Jc * lay.n_taps;
+  const double s_mac = std::sqrt(K) * (w_max / std::sqrt(3.0)) * s_rot;
+  double s_out = s_mac;
+  if (lay.cn == 2)
+    s_out = std::sqrt(2.0) * std::max((double)lay.k, 2.0 * std::fabs((double)lay.sign_coeff)) * s_mac +
+            (sh->depthwise ? 0.0 : s_rot);
+  else if (lay.cn == 4)
+    s_out = 2 * std::sqrt(3.0) * std::sqrt((double)N) * (t / std::sqrt(12.0)) * s_mac + std::sqrt(3.0) * s_rot;
+  *noise = std::log2(6 * s_out);
+  *budget = logQ - std::log2((double)t) - 1;
+  return HY_OK;
+}
+
+extern "C" hy_status hy_noise_estimate(uint32_t N, const uint64_t* q, uint32_t L, uint64_t t, const hy_conv_shape* sh,
+                                       uint32_t w_max, uint32_t w_dcmp, double* log2_noise, double* log2_budget) {
+  HY_CHECK(q && sh && log2_noise && log2_budget && L >= 1 && L <= HY_MAX_LIMBS, HY_EINVAL, "null argument");
+  return noise_model(N, q, L, t, sh, w_max, w_dcmp, log2_noise, log2_budget);
+}
+
+extern "C" hy_status hy_select_dcmp_base(uint32_t N, const uint64_t* q, uint32_t L, uint64_t t,
+                                         const hy_conv_shape* sh, uint32_t w_max, double margin_bits,
+                                         uint32_t* w_dcmp) {
+  HY_CHECK(q && sh && w_dcmp && L >= 1 && L <= HY_MAX_LIMBS, HY_EINVAL, "null argument");
+  uint32_t qbits = 0, qmin = 64;
+  for (uint32_t l = 0; l < L; l++) {
+    uint32_t b = 0;
+    while (b < 64 && (q[l] >> b)) b++;
+    qbits = std::max(qbits, b);
+    qmin = std::min(qmin, b);
+  }
+  // fewest digits first: V = 1 (one digit per limb), then the smallest w with V sub-digits
+  for (uint32_t V = 1; V <= 4 * HY_MAX_LIMBS / L; V++) {
+    const uint32_t w = V == 1 ? 0 : (qbits + V - 1) / V;
+    if (V > 1 && (w < 4 || w >= qmin)) continue;
+    double noise, budget;
+    HY_TRY(noise_model(N, q, L, t, sh, w_max, w, &noise, &budget));
+    if (budget - noise >= margin_bits) {
+      *w_dcmp = w;
+      return HY_OK;
+    }
+  }
+  hy_set_error("no decomposition base leaves %.1f bits of noise margin", margin_bits);
+  return HY_EINVAL;
 }
 
 // ============================================================================================

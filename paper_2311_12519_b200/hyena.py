@@ -17,7 +17,8 @@ __all__ = ["HyenaError", "hy_conv_shape", "hy_layout", "load_library", "library_
            "hy_weights_layout", "hy_weights_destroy", "hy_conv_eval", "hy_conv_eval_host", "hy_poly_mul",
            "hy_ntt_roundtrip", "hy_rotate", "hy_decrypt_debug", "hy_kernel_launches", "hy_weights_set_stage_events",
            "hy_weights_mac_time", "hy_weights_mac_path", "hy_weights_set_mac_path", "hy_secret_key", "hy_keygen",
-           "hy_encrypt", "hy_layout_accounting", "hy_accounting", "MAC_PATHS", "layout_dict", "EXPORTED"]
+           "hy_encrypt", "hy_layout_accounting", "hy_accounting", "hy_noise_estimate", "hy_select_dcmp_base",
+           "MAC_PATHS", "layout_dict", "EXPORTED"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 HY_MAX_TAPS = 49
@@ -29,7 +30,8 @@ EXPORTED = ["hy_last_error", "hy_plan_layout", "hy_params_create", "hy_params_cr
             "hy_encode_weights", "hy_weights_layout", "hy_weights_destroy", "hy_conv_eval", "hy_conv_eval_host",
             "hy_poly_mul", "hy_ntt_roundtrip", "hy_rotate", "hy_decrypt_debug", "hy_kernel_launches",
             "hy_weights_set_stage_events", "hy_weights_mac_time", "hy_weights_mac_path", "hy_weights_set_mac_path",
-            "hy_secret_key", "hy_keygen", "hy_encrypt", "hy_layout_accounting"]
+            "hy_secret_key", "hy_keygen", "hy_encrypt", "hy_layout_accounting", "hy_noise_estimate",
+            "hy_select_dcmp_base"]
 
 # S2 + S3 kernel choices (include/hyena.h hy_weights_mac_path)
 MAC_PATHS = {"thin": 0, "tc_fused": 1, "tc_split": 2, "fp64_fused": 3, "fp64_split": 4, "tc_coef": 5}
@@ -107,6 +109,10 @@ def load_library() -> ctypes.CDLL:
         "hy_weights_mac_path": (i32, [vp, ctypes.POINTER(i32)]),
         "hy_weights_set_mac_path": (i32, [vp, i32]),
         "hy_secret_key": (i32, [vp, u64, vp]),
+        "hy_noise_estimate": (i32, [u32, vp, u32, u64, ctypes.POINTER(hy_conv_shape), u32, u32,
+                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+        "hy_select_dcmp_base": (i32, [u32, vp, u32, u64, ctypes.POINTER(hy_conv_shape), u32, ctypes.c_double,
+                                      ctypes.POINTER(u32)]),
         "hy_layout_accounting": (i32, [ctypes.POINTER(hy_layout), ctypes.POINTER(hy_conv_shape), u32, u32,
                                        ctypes.POINTER(hy_accounting)]),
         "hy_keygen": (i32, [vp, u64, u32, vp, vp, ctypes.c_int]),
@@ -318,3 +324,24 @@ def hy_layout_accounting(lay: hy_layout, L: int, ND: int = 0, **shape) -> dict:
     _check(load_library().hy_layout_accounting(ctypes.byref(lay), ctypes.byref(s), L, ND or L, ctypes.byref(out)),
            "hy_layout_accounting")
     return {n: getattr(out, n) for n, _ in hy_accounting._fields_}
+
+
+def hy_noise_estimate(N: int, primes: Sequence[int], t: int, w_dcmp: int = 0, w_max: int = 128, **shape):
+    """(log2 noise estimate, log2 budget) of one layer (host only; include/hyena.h)."""
+    q = (ctypes.c_uint64 * len(primes))(*[int(x) for x in primes])
+    s = _shape(**shape)
+    nz, bd = ctypes.c_double(), ctypes.c_double()
+    _check(load_library().hy_noise_estimate(N, q, len(primes), t, ctypes.byref(s), w_max, w_dcmp, ctypes.byref(nz),
+                                            ctypes.byref(bd)), "hy_noise_estimate")
+    return nz.value, bd.value
+
+
+def hy_select_dcmp_base(N: int, primes: Sequence[int], t: int, margin_bits: float = 4.0, w_max: int = 128,
+                        **shape) -> int:
+    """The largest decomposition base (fewest key digits) leaving margin_bits of noise margin."""
+    q = (ctypes.c_uint64 * len(primes))(*[int(x) for x in primes])
+    s = _shape(**shape)
+    w = ctypes.c_uint32()
+    _check(load_library().hy_select_dcmp_base(N, q, len(primes), t, ctypes.byref(s), w_max, margin_bits,
+                                              ctypes.byref(w)), "hy_select_dcmp_base")
+    return w.value

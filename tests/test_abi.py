@@ -128,3 +128,27 @@ def test_layout_accounting_matches_paper_tables(hy):
     assert acc["input_ct_bytes"] == acc["output_ct_bytes"] == 4096 * 2 * 3 * 8192 * 8
     assert acc["rotations"] == 4096 * 8 and acc["n_keys"] == 8
     assert acc["coef_macs"] == 64 * 64 * 576 * 2 * 3 * 8192
+
+
+def test_noise_model_tracks_the_oracle(hy):
+    """The base-selection noise model (hy_noise_estimate) against the oracle's noise meter on C1 with
+    c_n = 2 and with c_n = 4 at two sub-digit bases: within 3 bits; hy_select_dcmp_base picks one
+    digit per limb for c_n = 2 and the 2^25 base (2 sub-digits per limb) for c_n = 4, which the oracle
+    confirms decrypts with >= 4 bits of margin (tests/test_oracle_conv.py: w = 20, 25; w = 0 fails)."""
+    from oracle import bfv
+    from tests.hyena_client import layer_from_config, make_layer
+    cfg = synth.configs()["C1"]
+    for cn, w in ((2, 0), (4, 25), (4, 20)):
+        if cn == 2:
+            lay = layer_from_config(cfg)
+        else:
+            lay = make_layer(cfg.N, cfg.primes, cfg.batch, cfg.Ci, cfg.Co, cfg.H, cfg.W, cfg.kh, cfg.kw, cfg.pad,
+                             seed=cfg.index, force_cn=4, x=synth.gen_image(cfg), Wt=synth.gen_weights(cfg), w=w)
+        out = conv.he_conv(lay.P, lay.ls, lay.W, lay.ct_in, lay.keys)
+        measured = max(bfv.noise_bits(lay.P, c, lay.s, bfv.decrypt(lay.P, c, lay.s)) for c in out.values())
+        shape = dict(cfg.shape_dict(), force_cn=cn)
+        est, budget = hy.hy_noise_estimate(cfg.N, cfg.primes, cfg.t, w_dcmp=w, w_max=8, **shape)
+        assert abs(est - measured) <= 3, (cn, w, est, measured)
+        assert abs(budget - bfv.noise_budget_bits(lay.P)) < 0.01
+    assert hy.hy_select_dcmp_base(cfg.N, cfg.primes, cfg.t, 4.0, 8, **cfg.shape_dict()) == 0
+    assert hy.hy_select_dcmp_base(cfg.N, cfg.primes, cfg.t, 4.0, 8, **dict(cfg.shape_dict(), force_cn=4)) == 25

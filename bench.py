@@ -294,7 +294,9 @@ MAC_KERNEL = {"thin": "ksmac_thin_kernel (fused S2+S3, FP64 MAC)",
               "tc_split": "mac_tc_kernel (S3 tcgen05 int8 MAC over stored R)",
               "fp64_fused": "ksmac_gemm_kernel (fused S2+S3, FP64 MAC)",
               "fp64_split": "mac_gemm_kernel (S3 FP64 MAC over stored R)",
-              "tc_coef": "ksmac_tc_kernel (1x1: tcgen05 int8 MAC on the coefficient-form input cts, no key switching)"}
+              "tc_coef": "ksmac_tc_kernel (1x1: tcgen05 int8 MAC on the coefficient-form input cts, no key switching)",
+              "eager": "mac_eager_kernel (ablation: lazy reduction off, one Shoup product per coefficient-MAC)",
+              "direct": "mac_tc_kernel after per-rotation decompositions (ablation: hoisting off)"}
 
 
 def roofline(cfg, res, peaks, steps):
@@ -332,10 +334,13 @@ def roofline(cfg, res, peaks, steps):
         a = w["modmul"][stage] / (st[stage] * 1e-3) / 1e9 if st[stage] > 0 else 0.0
         kernels[stage] = {"bound": "alu", "achieved": a, "peak": int_peak, "unit": "Gmodmul/s",
                           "frac": a / int_peak, "ms": st[stage]}
-    if path in ("tc_fused", "thin"):
+    if path == "eager":             # one modular product per coefficient-MAC (the ablation's bound)
+        a = w["coef_macs"] / (mac_ms * 1e-3) / 1e9
+        mac = {"bound": "alu", "achieved": a, "peak": int_peak, "unit": "Gmodmul/s", "frac": a / int_peak}
+    elif path in ("tc_fused", "thin"):
         a = w["modmul"]["S2S3_ksmac_wht"] / (mac_ms * 1e-3) / 1e9
         mac = {"bound": "alu", "achieved": a, "peak": int_peak, "unit": "Gmodmul/s", "frac": a / int_peak}
-    elif path in ("tc_split", "tc_coef"):
+    elif path in ("tc_split", "tc_coef", "direct"):
         hbm = peaks.get("hbm_gbs", 6546.6)
         a = (w["r_bytes"] + w["out_bytes"] * (2 if lay.cn == 2 and not cfg.depthwise else 1)) / (mac_ms * 1e-3) / 1e9
         mac = {"bound": "hbm", "achieved": a, "peak": hbm, "unit": "GB/s", "frac": a / hbm}

@@ -224,7 +224,13 @@ hy_status hy_weights_mac_time(const hy_weights* w, float* total_ms, uint32_t* la
  *   3 HY_MAC_FP64_FUSED  dense, M <= 32 (default there): key switching + FP64 DFMA MAC (30-bit halves);
  *   4 HY_MAC_FP64_SPLIT  dense, M > 32: PermAuto + FP64 DFMA MAC;
  *   5 HY_MAC_TC_COEF     1x1 kernel, pad 0, c_n = 1: tcgen05 MAC directly on the coefficient-form
- *                        inputs (identity tap, linear MAC), no NTT / INTT at all.
+ *                        inputs (identity tap, linear MAC), no NTT / INTT at all;
+ *   6 HY_MAC_EAGER       ablation "lazy reduction off" (Fig. 4 (d) vs (e), :718-728): PermAuto +
+ *                        a MAC that reduces after every product and addition (same residues);
+ *   7 HY_MAC_DIRECT      ablation "hoisting off" (Fig. 4 (b), :373-378): every rotation decomposes the
+ *                        rotated c1 again (its bits are the direct HRot's, not the hoisted one's:
+ *                        oracle bfv.rotate_direct), then the tcgen05 MAC.
+ * 6 and 7 are never chosen automatically (c_n <= 2, dense layers).
  * Every path computes the same bits (the MAC is exact integer arithmetic).  set_mac_path selects
  * another valid path for A/B measurement and parity tests (allocates the rotated-input workspace
  * of the split paths).  Errors: HY_EINVAL (path not valid for this layout), HY_ENOMEM. */

@@ -182,6 +182,28 @@ def rotate_hoisted(P: BFVParams, ct, digits, g: int, key) -> np.ndarray:
     return out
 
 
+def rotate_direct(P: BFVParams, ct, g: int, key) -> np.ndarray:
+    """HRot WITHOUT hoisting (the ablation of PAPER.md Fig. 4 (b), :373-378, :778-787): the
+    automorphism acts on every limb first (mod q_l), then the ROTATED c1 is decomposed (digits of
+    [sigma_g(c1)]_{q_i}), so every rotation repeats the decomposition.  Bitwise different from the
+    hoisted definition (reading R6), same decryption."""
+    L, N = P.L, P.N
+    rot = np.stack([np.stack([ring.automorphism_mod(ct[c, l], g, q) for l, q in enumerate(P.primes)])
+                    for c in range(2)])
+    digits = decompose(P, rot)
+    out = np.empty((2, L, N), dtype=np.uint64)
+    for l, q in enumerate(P.primes):
+        c0 = rot[0, l].astype(object)
+        c1 = np.zeros(N, dtype=object)
+        for i in range(len(digits)):
+            d = ring.canon(digits[i], q)
+            c0 = c0 + ring.nc_mul(d, key[i, 0, l], q).astype(object)
+            c1 = c1 + ring.nc_mul(d, key[i, 1, l], q).astype(object)
+        out[0, l] = (c0 % q).astype(np.uint64)
+        out[1, l] = (c1 % q).astype(np.uint64)
+    return out
+
+
 def hrot(P: BFVParams, ct, g: int, key) -> np.ndarray:
     """HRot by one automorphism (hoisted definition applied to a single rotation)."""
     return rotate_hoisted(P, ct, decompose(P, ct), g, key)

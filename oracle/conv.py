@@ -366,11 +366,12 @@ def _weight(Wt: np.ndarray, p: Plan, o: int, c: int, tau: int) -> int:
 
 
 def rotations(P: bfv.BFVParams, p: Plan, ct_in: np.ndarray, keys: Dict[int, np.ndarray],
-              units: Optional[List[int]] = None, cts: Optional[List[int]] = None
+              units: Optional[List[int]] = None, cts: Optional[List[int]] = None, hoisted: bool = True
               ) -> Dict[Tuple[int, int], np.ndarray]:
     """R[(ct, tau)]: every input ciphertext (of `units`, or exactly the ciphertexts `cts`) rotated
     by every tap step, hoisted (PermDecomp once per ciphertext, PermAuto per tap;
-    PAPER.md:375-377, 1590-1591)."""
+    PAPER.md:375-377, 1590-1591), or, for the no-hoisting ablation (Fig. 4 (b)), each rotation with
+    its own decomposition (bfv.rotate_direct)."""
     R = {}
     units = range(p.U) if units is None else units
     if cts is None:
@@ -383,7 +384,8 @@ def rotations(P: bfv.BFVParams, p: Plan, ct_in: np.ndarray, keys: Dict[int, np.n
                     R[(ci, tau)] = ct_in[ci].copy()
                 else:
                     g = galois_elt_for_step(p.N, s)
-                    R[(ci, tau)] = bfv.rotate_hoisted(P, ct_in[ci], digits, g, keys[g])
+                    R[(ci, tau)] = (bfv.rotate_hoisted(P, ct_in[ci], digits, g, keys[g]) if hoisted
+                                    else bfv.rotate_direct(P, ct_in[ci], g, keys[g]))
     return R
 
 

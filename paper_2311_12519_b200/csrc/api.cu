@@ -873,6 +873,8 @@ extern "C" hy_status hy_weights_set_mac_path(hy_weights* w, int32_t path) {
     case HY_MAC_FP64_SPLIT: ok = !dw && w->M > 32; break;  // 64-row FP64 tiles (hy_mac_mpad)
     case HY_MAC_FP64_FUSED: ok = !dw && w->M <= 32; break;
     case HY_MAC_TC_COEF: ok = coef_ok(w, w->lay); break;
+    case HY_MAC_EAGER: ok = !dw && !cn4; break;
+    case HY_MAC_DIRECT: ok = !dw && !cn4; break;
   }
   HY_CHECK(ok, HY_EINVAL, "MAC path %d is not valid for this layout (M = %d, L = %d, depthwise = %d)", path, w->M, L,
            (int)dw);
@@ -900,7 +902,31 @@ extern "C" hy_status hy_weights_set_mac_path(hy_weights* w, int32_t path) {
       w->d_C0 = nc;
     }
   }
-  const bool split = path == HY_MAC_TC_SPLIT || path == HY_MAC_FP64_SPLIT;
+  const bool split = path == HY_MAC_TC_SPLIT || path == HY_MAC_FP64_SPLIT || path == HY_MAC_EAGER ||
+                     path == HY_MAC_DIRECT;
+  if (path == HY_MAC_EAGER && !w->d_wq) {  // weights mod q_l with Shoup companions, [L][Kpad][Mpad] x 2
+    const size_t Lq = w->p->L, blk = (size_t)w->Kpad * w->Mpad;
+    std::vector<double> wt(blk);
+    if (cudaMemcpy(wt.data(), w->d_wt, blk * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess) {
+      hy_set_error("weight table read-back failed");
+      return HY_ECUDA;
+    }
+    std::vector<u64> wq(2 * Lq * blk);
+    for (size_t l = 0; l < Lq; l++) {
+      const u64 q = w->p->q[l];
+      for (size_t i = 0; i < blk; i++) {
+        const int64_t v = (int64_t)wt[i];
+        const u64 r = v >= 0 ? (u64)v % q : q - ((u64)(-v) % q);
+        wq[l * blk + i] = r;
+        wq[Lq * blk + l * blk + i] = shoup(r, q);
+      }
+    }
+    hy_status st = upload((void**)&w->d_wq, wq.data(), wq.size() * sizeof(u64));
+    if (st != HY_OK) {
+      w->d_wq = nullptr;
+      return st;
+    }
+  }
   if (split && !w->d_R) {
     const size_t words = (size_t)w->r_units * w->K * 2 * L * w->p->N;
     cudaError_t ce = cudaMalloc(&w->d_R, words * sizeof(u64));
@@ -934,6 +960,7 @@ extern "C" void hy_weights_destroy(hy_weights* w) {
   cudaFree(w->d_X);
   cudaFree(w->d_A1);
   cudaFree(w->d_R);
+  cudaFree(w->d_wq);
   cudaFree(w->d_in);
   cudaFree(w->d_out);
   if (w->s_h2d) {
@@ -1025,9 +1052,12 @@ extern "C" hy_status hy_conv_eval(hy_weights* w, const uint64_t* ct_in, size_t J
     HY_TRY(mark(3));
     return HY_OK;
   }
-  HY_TRY(hyk::permdecomp(p, ct_in, J, w->d_D, w->d_C0, s));  // S1 PermDecomp
+  if (w->mac_path == HY_MAC_DIRECT)  // no-hoisting ablation: only NTT(c0) here, digits per rotation
+    HY_TRY(hyk::c0_only(p, ct_in, J, w->d_C0, s));
+  else
+    HY_TRY(hyk::permdecomp(p, ct_in, J, w->d_D, w->d_C0, s));  // S1 PermDecomp
   HY_TRY(mark(1));
-  HY_TRY(hyk::ksmac(w, nu, s));  // S2 PermAuto fused with S3 lazy MAC + WHT + reduce + sign PMult
+  HY_TRY(hyk::ksmac(w, ct_in, nu, s));  // S2 PermAuto fused with S3 lazy MAC + WHT + reduce + sign PMult
   HY_TRY(mark(2));
   HY_TRY(hyk::finish_outputs(w, nu, ct_out, s));  // S4 alignment + S5 INTT
   HY_TRY(mark(3));

@@ -139,6 +139,8 @@ enum HyMacPath {
   HY_MAC_FP64_SPLIT = 4,  // A/B option HY_MAC_FP64 (M > 32): PermAuto + FP64 DFMA MAC
   HY_MAC_TC_COEF = 5,     // 1x1: tcgen05 MAC straight on the coefficient-form inputs (c_n = 1: no NTT;
                           // c_n = 2: only the row-swap alignment's NTTs)
+  HY_MAC_EAGER = 6,       // ablation "lazy reduction off" (Fig. 4 (d)): PermAuto + a MAC reducing every term
+  HY_MAC_DIRECT = 7,      // ablation "hoisting off" (Fig. 4 (b)): every rotation decomposes again, tcgen05 MAC
 };
 int hy_mac_path(int M, int L, bool depthwise, bool coef_ok, int cn, bool subdigits);
 
@@ -166,6 +168,7 @@ struct hy_weights {
   u64* d_X;         // [U*Jo][2][L][N] aligned outputs (NTT form) before the final INTT
   u64* d_A1;        // [U*Jo][2][2][L][N] [A1] of the coefficient-domain c_n = 2 1x1 path
   u64* d_R;         // [r_units][K][2][L][N] rotated inputs of the dense path (slot-order NTT)
+  u64* d_wq;        // HY_MAC_EAGER: [L][Kpad][Mpad] weights mod q_l, then the same block of Shoup companions
   int r_units;      // units per PermAuto + MAC batch
   cudaStream_t s_h2d, s_d2h;   // hy_conv_eval_host copy streams (created on first use)
   cudaEvent_t ev_h2d, ev_comp;
@@ -280,7 +283,8 @@ hy_status pointwise_mul(const hy_params* p, const u64* a, const u64* b, u64* c, 
 hy_status shoup_table(const hy_params* p, const u64* w, u64* w_sh, size_t npoly, cudaStream_t s);  // [n][L][N]
 hy_status key_to_ntt(const hy_params* p, const u64* key_coeff, u64* key_ntt, cudaStream_t s);
 hy_status permdecomp(const hy_params* p, const u64* ct, size_t nct, u64* D, u64* C0, cudaStream_t s);
-hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s);  // S2 + S3
+hy_status ksmac(hy_weights* w, const u64* ct_in, size_t nunits, cudaStream_t s);  // S2 + S3
+hy_status c0_only(const hy_params* p, const u64* ct, size_t nct, u64* C0, cudaStream_t s);  // NTT(c0) per limb
 hy_status finish_outputs(const hy_weights* w, size_t nunits, u64* ct_out, cudaStream_t s);
 hy_status mac_coef(hy_weights* w, const u64* ct_in, size_t nunits, u64* ct_out, cudaStream_t s);
 hy_status finish_coef2(const hy_weights* w, size_t nunits, u64* ct_out, cudaStream_t s);

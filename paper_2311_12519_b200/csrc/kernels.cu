@@ -61,8 +61,9 @@ struct PermDecompJob {
   bool red;
   int ND = 0, V = 1, wd = 0;  // gadget digits (0: ND = L), sub-digits per limb, base bits
   int sh = -1;                 // sub-digit shift of this job (-1: a whole residue)
+  bool c0_only = false;        // only NTT(c0) (the no-hoisting ablation decomposes per rotation)
   __device__ void bind(int b) {
-    const int nd = ND ? ND : L;
+    const int nd = c0_only ? 0 : (ND ? ND : L);
     const int per = nd * L + L;
     const int c = b / per, r = b % per;
     const u64* cb = ct + (size_t)c * (ct_stride ? ct_stride : (size_t)2 * L * N);
@@ -175,6 +176,7 @@ struct KsApplyArgs {
   size_t total;  // nout * L * N
   LimbConsts lcs;
   int ND = 0;    // gadget digits (0: ND = L, one per limb); D is [o][ND][L][N], keys [ND][2][L][N]
+  int d_rot = 0; // 1: D holds the digits of the already ROTATED c1 (no-hoisting ablation): read at j
 };
 
 template <int LT>
@@ -197,7 +199,7 @@ __global__ void __launch_bounds__(256) ks_apply_kernel(KsApplyArgs a) {
   u64 a0 = __ldg(a.c0 + o * a.c0_stride + (size_t)l * N + jp), a1 = 0;
   for (int i = 0; i < ND; i++) {
     const u64 dv = (a.diag && ND == L && i == l) ? __ldg(a.diag + o * a.diag_stride + (size_t)i * N + jp)
-                                                 : __ldg(D + ((size_t)i * L + l) * N + jp);
+                                                 : __ldg(D + ((size_t)i * L + l) * N + (a.d_rot ? j : jp));
     const u64* k0 = kb + (size_t)(2 * i) * LN;
     const u64* k1 = k0 + LN;
     a0 = csub(a0 + shoup_mul(dv, __ldg(k0), __ldg(k0 + kblk), q), q2);
@@ -225,6 +227,41 @@ hy_status launch_ks_apply(const KsApplyArgs& a, cudaStream_t s) {
   HY_LAUNCH_CHECK();
   return HY_OK;
 }
+
+// no-hoisting ablation (Fig. 4 (b)): digit dd (limb i, sub-digit v) of the ROTATED c1,
+// [sigma_g(c1)]_{q_i}[k] = +/- c1_i[k g^{-1} mod 2N] (mod q_i), NTT'd into limb l: D [c][ND][L][N]
+struct DirectDecompJob {
+  const u64* ct;   // [c][2][L][N] coefficient form
+  u64* D;
+  int L, N, ND, V, wd;
+  QArr qa;
+  uint32_t ginv;   // g^{-1} mod 2N
+  int limb;
+  const u64* s;
+  u64* d;
+  u64 qi, qd;
+  int sh;
+  bool red;
+  __device__ void bind(int b) {
+    const int c = b / (ND * L), r = b % (ND * L);
+    const int dd = r / L, i = dd / V;
+    limb = r % L;
+    s = ct + ((size_t)c * 2 * L + L + i) * N;
+    d = D + ((size_t)(c * ND + dd) * L + limb) * N;
+    qi = qa.q[i];
+    qd = qa.q[limb];
+    sh = V > 1 ? wd * (dd % V) : -1;
+    red = V > 1 ? false : qa.q[i] / 4 >= qa.q[limb];
+  }
+  __device__ u64 load(int k) const {
+    const uint32_t k0 = (uint32_t)(((uint64_t)k * ginv) % (2 * (uint64_t)N));
+    u64 x = k0 < (uint32_t)N ? s[k0] : s[k0 - N];
+    if (k0 >= (uint32_t)N) x = x ? qi - x : 0;
+    if (sh >= 0) return (x >> sh) & ((1ull << wd) - 1);
+    return red ? x % qd : x;
+  }
+  __device__ void store(int k, u64 v) const { d[k] = v; }
+};
 
 // plain INTT of an NTT-form ct array [o][cn'][2][L][N] picking diagonal 0 -> ct_out [o][2][L][N]
 struct OutInvJob {
@@ -483,6 +520,65 @@ __device__ __forceinline__ u64 ident_c1(const u64* D, int L, int ND, int wd, siz
     acc = (acc + mulmod_slow(__ldg(D + ((size_t)(l * V + v) * L + l) * N + j), (1ull << (wd * v)) % q, q)) % q;
   return acc;
 }
+
+// identity tap of the no-hoisting ablation: R = (NTT(c0), NTT(c1)) with NTT(c1) rebuilt from the
+// digits of the (unrotated) c1
+__global__ void ident_r_kernel(const u64* __restrict__ C0, const u64* __restrict__ D, u64* __restrict__ R, int nct,
+                               int L, int ND, int wd, int logN, QArr qa) {
+  const int N = 1 << logN;
+  const size_t total = (size_t)nct * L * N;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+    const int j = (int)(idx & (N - 1));
+    const size_t cl = idx >> logN;
+    const int l = (int)(cl % L), c = (int)(cl / L);
+    u64* r = R + (size_t)c * 2 * L * N + (size_t)l * N + j;
+    r[0] = C0[((size_t)c * L + l) * N + j];
+    r[(size_t)L * N] = ident_c1(D + (size_t)c * ND * L * N, L, ND, wd, N, l, j, qa.q[l]);
+  }
+}
+
+// lazy-reduction-off ablation (Fig. 4 (d)): the MAC over materialised R reducing after EVERY
+// product and addition ([acc + w R mod q] mod q), then the Walsh-Hadamard combination and the sign
+// PMult for c_n = 2 -- the same residues as the lazy MAC (P10), one Shoup product per coefficient-MAC
+__global__ void mac_eager_kernel(KsMacArgs a, const u64* __restrict__ R, const u64* __restrict__ wq, int units) {
+  const int N = 1 << a.logN, L = a.L;
+  const size_t LN = (size_t)L * N;
+  const int outs = a.cn == 2 ? a.M / 2 : a.M;  // P rows per unit
+  const size_t total = (size_t)units * outs * 2 * LN;
+  const size_t wblk = (size_t)L * a.Kpad * a.Mpad;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+    const int j = (int)(idx % N);
+    size_t r = idx / N;
+    const int l = (int)(r % L);
+    r /= L;
+    const int comp = (int)(r % 2);
+    r /= 2;
+    const int orow = (int)(r % outs), z = (int)(r / outs);
+    const LimbConst& c = a.lcs.lc[l];
+    const u64 q = c.q;
+    const u64* Rz = R + (size_t)z * a.K * 2 * LN + (size_t)comp * LN + (size_t)l * N + j;
+    const u64* wl = wq + (size_t)l * a.Kpad * a.Mpad;
+    const int nr = a.cn == 2 ? 2 : 1;
+    u64 B[2] = {0, 0};
+    for (int kk = 0; kk < a.K; kk++) {
+      const u64 x = __ldg(Rz + (size_t)kk * 2 * LN);
+      for (int rr = 0; rr < nr; rr++) {
+        const size_t wi = (size_t)kk * a.Mpad + (size_t)orow * nr + rr;
+        const u64 t = csub(shoup_mul(x, __ldg(wl + wi), __ldg(wl + wblk + wi), q), q);
+        B[rr] = csub(B[rr] + t, q);
+      }
+    }
+    u64 v = B[0];
+    if (a.cn == 2) {
+      const u64 a0 = mulmod_slow(csub(B[0] + B[1], q), (u64)a.kscale % q, q);
+      const u64 a1 = csub(B[0] + q - B[1], q);
+      v = csub(csub(a0 + shoup_mul(a1, __ldg(a.sign + (size_t)l * N + j), __ldg(a.sign + LN + (size_t)l * N + j), q),
+                    c.two_q), q);
+    }
+    a.out[((size_t)(z * outs + orow) * 2 + comp) * LN + (size_t)l * N + j] = v;
+  }
+}
+
 
 constexpr uint32_t M30 = 0x3FFFFFFFu;
 
@@ -2197,6 +2293,12 @@ hy_status key_to_ntt(const hy_params* p, const u64* key_coeff, u64* key_ntt, cud
   return HY_OK;
 }
 
+hy_status c0_only(const hy_params* p, const u64* ct, size_t nct, u64* C0, cudaStream_t s) {
+  PermDecompJob j{ct, nullptr, C0, (int)p->L, (int)p->N, qarr(p)};
+  j.c0_only = true;
+  return launch_fwd(p, j, nct * p->L, s);
+}
+
 hy_status permdecomp(const hy_params* p, const u64* ct, size_t nct, u64* D, u64* C0, cudaStream_t s) {
   PermDecompJob j{ct, D, C0, (int)p->L, (int)p->N, qarr(p)};
   j.ND = (int)p->ND;
@@ -2220,7 +2322,53 @@ static hy_status mac_mark(hy_weights* w, cudaStream_t s) {
   return HY_OK;
 }
 
-hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
+// no-hoisting ablation: rotated inputs R of units u0 .. u0 + nb - 1 by every tap, each rotation with its
+// own decomposition of the rotated c1 (DirectDecompJob) and key inner product (ks_apply, d_rot)
+static hy_status direct_rotations(hy_weights* w, const u64* ct_in, int u0, int nb, cudaStream_t s) {
+  const hy_params* p = w->p;
+  const hy_layout& lay = w->lay;
+  const size_t L = p->L, N = p->N, LN = L * N, Jc = lay.Jc, ctw = 2 * LN;
+  const u64 M2 = 2 * (u64)N;
+  for (int zb = 0; zb < nb; zb++) {
+    const size_t z = (size_t)u0 + zb;
+    for (uint32_t tau = 0; tau < lay.n_taps; tau++) {
+      const int64_t st = (((int64_t)lay.tap_step[tau] % (int64_t)(N / 2)) + N / 2) % (N / 2);
+      const u64 g = hyhost::powmod(3, (u64)st, M2), ginv = hyhost::powmod(g, N - 1, M2);  // |Z_2N^*| = N
+      DirectDecompJob jd{ct_in + z * Jc * ctw, w->d_D, (int)L, (int)N, (int)p->ND, (int)p->V, (int)p->w_dcmp,
+                         qarr(p), (uint32_t)ginv};
+      HY_TRY(launch_fwd(p, jd, Jc * p->ND * L, s));
+      u64* R = w->d_R + ((size_t)zb * w->K + (size_t)tau * Jc) * ctw;
+      if (w->h_tap_keys[tau] == nullptr) {
+        ident_r_kernel<<<148 * 4, 256, 0, s>>>(w->d_C0 + z * Jc * LN, w->d_D, R, (int)Jc, (int)L, (int)p->ND,
+                                                (int)p->w_dcmp, (int)p->logN, qarr(p));
+        HY_LAUNCH_CHECK();
+        continue;
+      }
+      KsApplyArgs ka;
+      ka.ND = (int)p->ND;
+      ka.d_rot = 1;
+      ka.c0 = w->d_C0 + z * Jc * LN;
+      ka.c0_stride = LN;
+      ka.D = w->d_D;
+      ka.D_stride = p->ND * LN;
+      ka.diag = nullptr;
+      ka.diag_stride = 0;
+      ka.add = nullptr;
+      ka.add_stride = 0;
+      ka.key = w->h_tap_keys[tau];
+      ka.act = w->h_tap_act[tau];
+      ka.out = R;
+      ka.L = (int)L;
+      ka.logN = (int)p->logN;
+      ka.total = Jc * LN;
+      ka.lcs = limb_consts(p);
+      HY_TRY(launch_ks_apply(ka, s));
+    }
+  }
+  return HY_OK;
+}
+
+hy_status ksmac(hy_weights* w, const u64* ct_in, size_t nunits, cudaStream_t s) {
   w->mac_launches = 0;
   const hy_params* p = w->p;
   const hy_layout& lay = w->lay;
@@ -2294,18 +2442,26 @@ hy_status ksmac(hy_weights* w, size_t nunits, cudaStream_t s) {
     b.D = a.D + (size_t)u0 * a.Jcb * p->ND * LN;
     b.C0 = a.C0 + (size_t)u0 * a.Jcb * LN;
     b.out = a.out + (size_t)u0 * mrows * 2 * LN;
-    switch (Lsel) {
-      case 2: HY_TRY(launch_permauto<2>(b, w->d_R, nb, s)); break;
-      case 3: HY_TRY(launch_permauto<3>(b, w->d_R, nb, s)); break;
-      case 5: HY_TRY(launch_permauto<5>(b, w->d_R, nb, s)); break;
-      default: HY_TRY(launch_permauto<0>(b, w->d_R, nb, s)); break;
+    if (path == HY_MAC_DIRECT) {
+      HY_TRY(direct_rotations(w, ct_in, u0, nb, s));
+    } else {
+      switch (Lsel) {
+        case 2: HY_TRY(launch_permauto<2>(b, w->d_R, nb, s)); break;
+        case 3: HY_TRY(launch_permauto<3>(b, w->d_R, nb, s)); break;
+        case 5: HY_TRY(launch_permauto<5>(b, w->d_R, nb, s)); break;
+        default: HY_TRY(launch_permauto<0>(b, w->d_R, nb, s)); break;
+      }
     }
     HY_TRY(mac_mark(w, s));
     if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[2 * w->mac_launches], s));
-    if (fp64_mac)
+    if (path == HY_MAC_EAGER) {
+      mac_eager_kernel<<<148 * 16, 256, 0, s>>>(b, w->d_R, w->d_wq, nb);
+      HY_LAUNCH_CHECK();
+    } else if (fp64_mac) {
       HY_TRY(launch_mac_gemm<8>(b, w->d_R, nb, s));
-    else
+    } else {
       HY_TRY(launch_mac_tc(b, w->d_R, w->d_w8, nb, s));
+    }
     if (w->n_ev) HY_CUDA_TRY(cudaEventRecord((*w->mac_ev)[2 * w->mac_launches + 1], s));
     w->mac_launches++;
   }

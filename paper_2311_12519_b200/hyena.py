@@ -34,7 +34,8 @@ EXPORTED = ["hy_last_error", "hy_plan_layout", "hy_params_create", "hy_params_cr
             "hy_select_dcmp_base"]
 
 # S2 + S3 kernel choices (include/hyena.h hy_weights_mac_path)
-MAC_PATHS = {"thin": 0, "tc_fused": 1, "tc_split": 2, "fp64_fused": 3, "fp64_split": 4, "tc_coef": 5}
+MAC_PATHS = {"thin": 0, "tc_fused": 1, "tc_split": 2, "fp64_fused": 3, "fp64_split": 4, "tc_coef": 5,
+             "eager": 6, "direct": 7}
 
 
 class HyenaError(RuntimeError):

@@ -94,7 +94,8 @@ def test_hoisted_vs_direct_differ_but_decrypt_equal():
     g = galois_elt_for_step(P.N, 1)
     key = _key(P, s, g, 4)
     hoisted = bfv.hrot(P, ct, g, key)
-    # direct: automorphism on every limb first, then digits of the rotated c1 in [0, q_i)
+    # direct: automorphism on every limb first, then digits of the rotated c1 in [0, q_i) (written
+    # out here, independently of bfv.rotate_direct, which must agree)
     rot = np.stack([np.stack([ring.automorphism_mod(ct[c, l], g, q) for l, q in enumerate(P.primes)])
                     for c in range(2)])
     direct = np.empty_like(rot)
@@ -107,6 +108,7 @@ def test_hoisted_vs_direct_differ_but_decrypt_equal():
             c1 = c1 + ring.nc_mul(d, key[i, 1, l], q).astype(object)
         direct[0, l] = (c0 % q).astype(np.uint64)
         direct[1, l] = (c1 % q).astype(np.uint64)
+    assert np.array_equal(bfv.rotate_direct(P, ct, g, key), direct)
     assert not np.array_equal(hoisted, direct)
     assert list(bfv.decrypt(P, hoisted, s)) == list(bfv.decrypt(P, direct, s))
 

@@ -25,6 +25,12 @@ QArr qarr(const hy_params* p) {
   return a;
 }
 
+QArr onesh_arr(const hy_params* p) {  // floor(2^64 / q_l): x mod q_l in [0, 2 q_l) by one Shoup product
+  QArr a;
+  for (uint32_t l = 0; l < p->L; l++) a.q[l] = p->lc[l].one_sh;
+  return a;
+}
+
 // ------------------------------------------------------------------------------------------
 // NTT jobs
 // ------------------------------------------------------------------------------------------
@@ -45,8 +51,8 @@ struct PolyJob {  // src/dst [n][L][N]; `src_stride_polys` lets a job walk every
 };
 
 // S1 PermDecomp (PAPER.md:375-377, :1472 [app]): per input ct, digits d_i = [c1]_{q_i} lifted to
-// every limb l and NTT'd (ND*L jobs), plus NTT(c0) per limb (L jobs).  With a sub-digit base 2^w
-// (hy_params_create2, NEXT-4) digit dd = i V + v is floor(d_i / 2^{w v}) mod 2^w (< 2^w < q_l).
+// every limb l and NTT'd (L*L jobs), plus NTT(c0) per limb (L jobs).  (c0_only: the L NTT(c0) jobs
+// alone, for the no-hoisting ablation; PermDecompSubJob: the sub-digit base variant.)
 struct PermDecompJob {
   const u64* ct;
   u64* D;
@@ -59,23 +65,19 @@ struct PermDecompJob {
   u64* d;
   u64 qd;
   bool red;
-  int ND = 0, V = 1, wd = 0;  // gadget digits (0: ND = L), sub-digits per limb, base bits
-  int sh = -1;                 // sub-digit shift of this job (-1: a whole residue)
-  bool c0_only = false;        // only NTT(c0) (the no-hoisting ablation decomposes per rotation)
+  bool c0_only = false;
   __device__ void bind(int b) {
-    const int nd = c0_only ? 0 : (ND ? ND : L);
+    const int nd = c0_only ? 0 : L;
     const int per = nd * L + L;
     const int c = b / per, r = b % per;
     const u64* cb = ct + (size_t)c * (ct_stride ? ct_stride : (size_t)2 * L * N);
-    sh = -1;
     if (r < nd * L) {
-      const int dd = r / L, i = dd / V;
+      const int i = r / L;
       limb = r % L;
       s = cb + ((size_t)L + i) * N;
-      d = D + ((size_t)(c * nd + dd) * L + limb) * N;
+      d = D + ((size_t)(c * L + i) * L + limb) * N;
       qd = qa.q[limb];
-      if (V > 1) sh = wd * (dd % V);
-      red = V > 1 ? false : qa.q[i] / 4 >= qa.q[limb];  // digit may exceed the lazy [0, 4 q_l) range
+      red = qa.q[i] / 4 >= qa.q[limb];  // digit may exceed the lazy [0, 4 q_l) input range
     } else {
       limb = r - nd * L;
       s = cb + (size_t)limb * N;
@@ -86,8 +88,43 @@ struct PermDecompJob {
   }
   __device__ u64 load(int k) const {
     u64 x = s[k];
-    if (sh >= 0) return (x >> sh) & ((1ull << wd) - 1);
     return red ? x % qd : x;
+  }
+  __device__ void store(int k, u64 v) const { d[k] = v; }
+};
+
+// PermDecomp with a sub-digit base 2^w (hy_params_create2, NEXT-4): digit dd = i V + v of limb i is
+// floor([c1]_{q_i} / 2^{w v}) mod 2^w (< q_l), NTT'd into every limb l (ND*L jobs) + NTT(c0) (L jobs)
+struct PermDecompSubJob {
+  const u64* ct;
+  u64* D;
+  u64* C0;
+  int L, N, ND, V, wd;
+  size_t ct_stride;
+  int limb;
+  const u64* s;
+  u64* d;
+  int sh;  // -1: c0 (whole residue)
+  __device__ void bind(int b) {
+    const int per = ND * L + L;
+    const int c = b / per, r = b % per;
+    const u64* cb = ct + (size_t)c * (ct_stride ? ct_stride : (size_t)2 * L * N);
+    if (r < ND * L) {
+      const int dd = r / L;
+      limb = r % L;
+      s = cb + ((size_t)L + dd / V) * N;
+      d = D + ((size_t)(c * ND + dd) * L + limb) * N;
+      sh = wd * (dd % V);
+    } else {
+      limb = r - ND * L;
+      s = cb + (size_t)limb * N;
+      d = C0 + ((size_t)c * L + limb) * N;
+      sh = -1;
+    }
+  }
+  __device__ u64 load(int k) const {
+    const u64 x = s[k];
+    return sh >= 0 ? (x >> sh) & ((1ull << wd) - 1) : x;
   }
   __device__ void store(int k, u64 v) const { d[k] = v; }
 };
@@ -118,6 +155,7 @@ struct DigitLiftJob {
   u64* D2;         // [o][ND digit][L limb][N]
   int L, N;
   QArr qa;
+  QArr osh{};  // floor(2^64 / q_l) per limb (onesh_arr)
   int limb;
   const u64* s;
   u64* d;
@@ -150,7 +188,7 @@ struct DigitLiftJob {
   __device__ u64 load(int k) const {
     u64 x = s[k];
     if (ND) return (x >> sh) & ((1ull << wd) - 1);
-    return red ? x % qd : x;
+    return red ? reduce_2q(x, osh.q[limb], qd) : x;  // [0, 2 q_l): inside the NTT's [0, 4q) input
   }
   __device__ void store(int k, u64 v) const { d[k] = v; }
 };
@@ -235,6 +273,7 @@ struct DirectDecompJob {
   u64* D;
   int L, N, ND, V, wd;
   QArr qa;
+  QArr osh{};  // floor(2^64 / q_l) per limb (onesh_arr)
   uint32_t ginv;   // g^{-1} mod 2N
   int limb;
   const u64* s;
@@ -258,7 +297,7 @@ struct DirectDecompJob {
     u64 x = k0 < (uint32_t)N ? s[k0] : s[k0 - N];
     if (k0 >= (uint32_t)N) x = x ? qi - x : 0;
     if (sh >= 0) return (x >> sh) & ((1ull << wd) - 1);
-    return red ? x % qd : x;
+    return red ? reduce_2q(x, osh.q[limb], qd) : x;  // [0, 2 q_l): inside the NTT's [0, 4q) input
   }
   __device__ void store(int k, u64 v) const { d[k] = v; }
 };
@@ -620,12 +659,16 @@ __device__ __forceinline__ void ks_pair_regs(const u64* __restrict__ D, const u6
   u64 dv[LT];
 #pragma unroll
   for (int i = 0; i < LT; i++) dv[i] = __ldg(D + ((size_t)i * LT + l) * N + jp);
-  u64 a0 = __ldg(C0 + (size_t)l * N + jp), a1 = 0;
+  u64 a0 = __ldg(C0 + (size_t)l * N + jp), a1 = 0, h0 = 0, h1 = 0;
 #pragma unroll
-  for (int i = 0; i < LT; i++) {  // lazy: < (2L + 1) q < 2^64, one reduction per component
-    a0 += shoup_mul(dv[i], k.v[2 * i], k.sh[2 * i], q);
-    a1 += shoup_mul(dv[i], k.v[2 * i + 1], k.sh[2 * i + 1], q);
+  for (int i = 0; i < LT; i++) {  // lazy: < (2L + 1) q < 2^64, one quotient multiply + reduction each
+    a0 += dv[i] * k.v[2 * i];
+    h0 += __umul64hi(dv[i], k.sh[2 * i]);
+    a1 += dv[i] * k.v[2 * i + 1];
+    h1 += __umul64hi(dv[i], k.sh[2 * i + 1]);
   }
+  a0 -= h0 * q;
+  a1 -= h1 * q;
   r0 = csub(reduce_2q(a0, c.one_sh, q), q);
   r1 = csub(reduce_2q(a1, c.one_sh, q), q);
 }
@@ -874,11 +917,16 @@ __global__ void __launch_bounds__(256, 2) ksmac_gemm_kernel(KsMacArgs a) {
           r1 = pre[h].d[0];
         } else {
           const u64* kp = skey + (size_t)tap * 4 * NL * BNP + p_own;
+          u64 q0 = 0, q1 = 0;  // summed Shoup quotients: one quotient multiply per component
 #pragma unroll
           for (int i = 0; i < NL; i++) {  // lazy sums, one canonical reduction each
-            r0 += shoup_mul(pre[h].d[i], kp[(4 * i) * BNP], kp[(4 * i + 1) * BNP], q);
-            r1 += shoup_mul(pre[h].d[i], kp[(4 * i + 2) * BNP], kp[(4 * i + 3) * BNP], q);
+            r0 += pre[h].d[i] * kp[(4 * i) * BNP];
+            q0 += __umul64hi(pre[h].d[i], kp[(4 * i + 1) * BNP]);
+            r1 += pre[h].d[i] * kp[(4 * i + 2) * BNP];
+            q1 += __umul64hi(pre[h].d[i], kp[(4 * i + 3) * BNP]);
           }
+          r0 -= q0 * q;
+          r1 -= q1 * q;
           r0 = reduce_lazy_sum<NL>(r0, q);  // canonical: the 30-bit split needs R < 2^60
           r1 = reduce_lazy_sum<NL>(r1, q);
         }
@@ -1034,12 +1082,16 @@ __global__ void __launch_bounds__(256) ksmac_thin_kernel(KsMacArgs a, int units)
           r1 = dv[u][0];
         } else {
           const u64 q = cst.q, q2 = cst.two_q;
-          u64 x0 = c0v[u], x1 = 0;
+          u64 x0 = c0v[u], x1 = 0, g0 = 0, g1 = 0;
 #pragma unroll
-          for (int i = 0; i < LT; i++) {  // lazy sums, one canonical reduction each
-            x0 += shoup_mul(dv[u][i], kr.v[2 * i], kr.sh[2 * i], q);
-            x1 += shoup_mul(dv[u][i], kr.v[2 * i + 1], kr.sh[2 * i + 1], q);
+          for (int i = 0; i < LT; i++) {  // lazy sums (summed quotients), one canonical reduction each
+            x0 += dv[u][i] * kr.v[2 * i];
+            g0 += __umul64hi(dv[u][i], kr.sh[2 * i]);
+            x1 += dv[u][i] * kr.v[2 * i + 1];
+            g1 += __umul64hi(dv[u][i], kr.sh[2 * i + 1]);
           }
+          x0 -= g0 * q;
+          x1 -= g1 * q;
           r0 = reduce_lazy_sum<LT>(x0, q);  // canonical: the 30-bit split needs R < 2^60
           r1 = reduce_lazy_sum<LT>(x1, q);
         }
@@ -1127,12 +1179,16 @@ __global__ void __launch_bounds__(256) permauto_kernel(KsMacArgs a, u64* __restr
       // lazy: each Shoup product is in [0, 2q); c0 + sum < (2L + 1) q < 2^64 for q < 2^60, L <= 7;
       // one reduction per component
       const u64 q = cst.q;
-      u64 a0 = c0, a1 = 0;
+      u64 a0 = c0, a1 = 0, g0 = 0, g1 = 0;
 #pragma unroll
-      for (int i = 0; i < LT; i++) {
-        a0 += shoup_mul(d[i], kr.v[2 * i], kr.sh[2 * i], q);
-        a1 += shoup_mul(d[i], kr.v[2 * i + 1], kr.sh[2 * i + 1], q);
+      for (int i = 0; i < LT; i++) {  // summed Shoup quotients: one quotient multiply per component
+        a0 += d[i] * kr.v[2 * i];
+        g0 += __umul64hi(d[i], kr.sh[2 * i]);
+        a1 += d[i] * kr.v[2 * i + 1];
+        g1 += __umul64hi(d[i], kr.sh[2 * i + 1]);
       }
+      a0 -= g0 * q;
+      a1 -= g1 * q;
       __stcs(out + (size_t)c * 2 * LN, csub(reduce_2q(a0, cst.one_sh, q), q));
       __stcs(out + (size_t)c * 2 * LN + LN, csub(reduce_2q(a1, cst.one_sh, q), q));
     }
@@ -2300,11 +2356,12 @@ hy_status c0_only(const hy_params* p, const u64* ct, size_t nct, u64* C0, cudaSt
 }
 
 hy_status permdecomp(const hy_params* p, const u64* ct, size_t nct, u64* D, u64* C0, cudaStream_t s) {
+  if (p->ND != p->L) {
+    PermDecompSubJob j{ct, D, C0, (int)p->L, (int)p->N, (int)p->ND, (int)p->V, (int)p->w_dcmp, 0};
+    return launch_fwd(p, j, nct * (p->ND * p->L + p->L), s);
+  }
   PermDecompJob j{ct, D, C0, (int)p->L, (int)p->N, qarr(p)};
-  j.ND = (int)p->ND;
-  j.V = (int)p->V;
-  j.wd = (int)p->w_dcmp;
-  return launch_fwd(p, j, nct * (p->ND * p->L + p->L), s);
+  return launch_fwd(p, j, nct * (p->L * p->L + p->L), s);
 }
 
 // MAC-kernel timing (bench): record an event before/after each MAC launch when enabled
@@ -2335,7 +2392,7 @@ static hy_status direct_rotations(hy_weights* w, const u64* ct_in, int u0, int n
       const int64_t st = (((int64_t)lay.tap_step[tau] % (int64_t)(N / 2)) + N / 2) % (N / 2);
       const u64 g = hyhost::powmod(3, (u64)st, M2), ginv = hyhost::powmod(g, N - 1, M2);  // |Z_2N^*| = N
       DirectDecompJob jd{ct_in + z * Jc * ctw, w->d_D, (int)L, (int)N, (int)p->ND, (int)p->V, (int)p->w_dcmp,
-                         qarr(p), (uint32_t)ginv};
+                         qarr(p), onesh_arr(p), (uint32_t)ginv};
       HY_TRY(launch_fwd(p, jd, Jc * p->ND * L, s));
       u64* R = w->d_R + ((size_t)zb * w->K + (size_t)tau * Jc) * ctw;
       if (w->h_tap_keys[tau] == nullptr) {
@@ -2558,11 +2615,14 @@ hy_status finish_coef2(const hy_weights* w, size_t nunits, u64* ct_out, cudaStre
                         dim3(256), 0, s, 1, w->d_P, (const u64*)w->d_A1, total, (int)p->logN, (int)L,
                         limb_consts(p), sv, svsh));
   HY_LAUNCH_CHECK();
-  PermDecompJob jd{w->d_P + ctw, w->d_D, w->d_C0, (int)L, (int)N, qarr(p), 2 * ctw};  // P_1 of every output
-  jd.ND = (int)p->ND;
-  jd.V = (int)p->V;
-  jd.wd = (int)p->w_dcmp;
-  HY_TRY(launch_fwd(p, jd, nout * (p->ND * L + L), s));
+  if (p->ND != L) {  // P_1 of every output
+    PermDecompSubJob jd{w->d_P + ctw, w->d_D, w->d_C0, (int)L, (int)N, (int)p->ND, (int)p->V, (int)p->w_dcmp,
+                        2 * ctw};
+    HY_TRY(launch_fwd(p, jd, nout * (p->ND * L + L), s));
+  } else {
+    PermDecompJob jd{w->d_P + ctw, w->d_D, w->d_C0, (int)L, (int)N, qarr(p), 2 * ctw};
+    HY_TRY(launch_fwd(p, jd, nout * (L * L + L), s));
+  }
   KsApplyArgs ka;
   ka.ND = (int)p->ND;
   ka.c0 = w->d_C0;
@@ -2597,7 +2657,7 @@ static hy_status rotate_partials(const hy_weights* w, size_t nout, const u64* Pd
   u64* dig = w->d_D2 + nout * ND * L * N;  // [o][L][N] scratch after the digit NTTs
   StridedInvJob ja{Pd + L * N, pstride, dig, (int)L, (int)N};
   HY_TRY(launch_inv(p, ja, nout * L, s));
-  DigitLiftJob jb{dig, w->d_D2, (int)L, (int)N, qarr(p)};
+  DigitLiftJob jb{dig, w->d_D2, (int)L, (int)N, qarr(p), onesh_arr(p)};
   if (sub) {
     jb.ND = (int)ND;
     jb.V = (int)p->V;

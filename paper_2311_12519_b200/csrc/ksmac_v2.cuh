@@ -270,14 +270,18 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
       } else {
         const uint32_t kp = sm_a + geo.off_key + (uint32_t)(cit % 3) * geo.key_bytes + (uint32_t)pos * 8 +
                             (uint32_t)grp * (4 * LT * TC_POS * 8);
-        u64 r0[4], r1[4];
+        // lazy Shoup sums with ONE quotient multiply per component: sum_i (d_i w_i - h_i q) =
+        // sum_i d_i w_i - (sum_i h_i) q (mod 2^64), h_i = floor(d_i w'_i / 2^64); the true value is
+        // c0 + sum of L Shoup products in [0, 2q) < (2L + 1) q < 2^64, so the mod-2^64 result is
+        // exact and bit-identical to the per-product form (2 (L - 1) fewer 64-bit products per term)
+        u64 r0[4], r1[4], h0[4], h1[4];
 #pragma unroll
         for (int t = 0; t < 4; t++) {
           r0[t] = cur[t].c0;
-          r1[t] = 0;
+          r1[t] = h0[t] = h1[t] = 0;
         }
 #pragma unroll
-        for (int i = 0; i < LT; i++) {  // lazy: Shoup products in [0, 2q), R < (2L + 1) q < 2^64
+        for (int i = 0; i < LT; i++) {
           u64 kv, ksh, av, ash;
           asm volatile("ld.shared.u64 %0, [%1];" : "=l"(kv) : "r"(kp + (4 * i) * TC_POS * 8));
           asm volatile("ld.shared.u64 %0, [%1];" : "=l"(ksh) : "r"(kp + (4 * i + 1) * TC_POS * 8));
@@ -285,9 +289,17 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
           asm volatile("ld.shared.u64 %0, [%1];" : "=l"(ash) : "r"(kp + (4 * i + 3) * TC_POS * 8));
 #pragma unroll
           for (int t = 0; t < 4; t++) {
-            r0[t] += shoup_mul(cur[t].d[i], kv, ksh, q);
-            r1[t] += shoup_mul(cur[t].d[i], av, ash, q);
+            const u64 d = cur[t].d[i];
+            r0[t] += d * kv;
+            h0[t] += __umul64hi(d, ksh);
+            r1[t] += d * av;
+            h1[t] += __umul64hi(d, ash);
           }
+        }
+#pragma unroll
+        for (int t = 0; t < 4; t++) {
+          r0[t] -= h0[t] * q;
+          r1[t] -= h1[t] * q;
         }
 #pragma unroll
         for (int t = 0; t < 4; t++) {

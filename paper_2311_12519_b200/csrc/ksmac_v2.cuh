@@ -79,18 +79,17 @@ inline V2Geom v2_geom(int T, int L, int Kpad, size_t smem_max) {
 __device__ __forceinline__ void v2_cp16(uint32_t saddr, const void* g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(saddr), "l"(g) : "memory");
 }
-// mbarrier wait with a back-off: for the warps that idle most of the time (epilogue, UMMA issuer),
-// so that their polling does not take issue slots from the producers
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity, int ns) {
+// mbarrier wait that SUSPENDS the warp until the phase completes (try_wait with a suspend-time hint)
+// instead of polling: the epilogue and UMMA-issuer warps idle most of the time and their polling took
+// a quarter of the issue slots (profiled); the producers' waits use it too
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity, int /*ns*/) {
   uint32_t done = 0;
-  while (true) {
+  while (!done) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.b32 %0, 1, 0, p;\n\t}"
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.b32 %0, 1, 0, p;\n\t}"
         : "=r"(done)
-        : "r"(smem_u32(b)), "r"(parity)
+        : "r"(smem_u32(b)), "r"(parity), "r"(1000000u)
         : "memory");
-    if (done) break;
-    __nanosleep(ns);
   }
 }
 
@@ -249,10 +248,10 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
       if (cch == 0) {  // a new tile: its keys must have landed; prefetch those of tile cit + 2
         q = a.lcs.lc[((blockIdx.x + cit * gridDim.x) % per_unit) / tiles_pl].q;
         if (cit + 2 < my_tiles) {  // buffer (cit + 2) % 3 was last read by tile cit - 1
-          if (cit >= 1) mbar_wait(&kempty[(cit + 2) % 3], ((cit - 1) / 3) & 1);
+          if (cit >= 1) mbar_wait_sleep(&kempty[(cit + 2) % 3], ((cit - 1) / 3) & 1, 0);
           issue_keys(cit + 2);
         }
-        mbar_wait(&kfull[cit % 3], (cit / 3) & 1);
+        mbar_wait_sleep(&kfull[cit % 3], (cit / 3) & 1, 0);
       }
       if (gc + 1 < my_tiles * nchunks) load(nxt, grp_nxt);
       uint32_t lo0[4], hi0[4], lo1[4], hi1[4];
@@ -319,7 +318,7 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
       byte_tr4(lo1, p1);
       byte_tr4(hi1, p1 + 4);
       const int s = gc % S;
-      if (gc >= S) mbar_wait(&empty_bar[s], ((gc / S) - 1) & 1);
+      if (gc >= S) mbar_wait_sleep(&empty_bar[s], ((gc / S) - 1) & 1, 0);
       if (V2_KS * cch + ks < nk32) {
         const uint32_t bb = sm_a + geo.off_b + (uint32_t)s * V2_STAGE_B + (uint32_t)ks * 8192;
 #pragma unroll

@@ -100,6 +100,12 @@ CASES = {
     "one_pixel": dict(N=1024, bits=50, L=2, batch=1, Ci=1, Co=1, H=1, W=1, kh=3, kw=3, pad=1),
     "pw_one_channel": dict(N=1024, bits=50, L=2, batch=3, Ci=1, Co=1, H=5, W=5, kh=1, kw=1, pad=0),
     "k7x7": dict(N=1024, bits=50, L=2, batch=1, Ci=2, Co=3, H=3, W=3, kh=7, kw=7, pad=3),
+    # the persistent warp-specialised kernel (Jc % 4 == 0): c_n = 1 with 2 epilogue warps (M <= 64) and
+    # c_n = 2 with a ragged K (K = 36 -> 2 K steps of 32, the second 4 terms long)
+    "tc_v2_cn1": dict(N=1024, bits=50, L=3, batch=17, Ci=4, Co=40, H=6, W=6, kh=3, kw=3, pad=1,
+                      xrange=(-128, 128), wrange=(-128, 128)),
+    "tc_v2_cn2_rows96": dict(N=1024, bits=50, L=2, batch=1, Ci=8, Co=48, H=6, W=6, kh=3, kw=3, pad=1,
+                             xrange=(-128, 128), wrange=(-128, 128)),
     # K = Jc * 9 = 297 terms: 5 chunks of 64 with a ragged last K step; 128 rows exactly
     "tc_cn2_k297_rows128": dict(N=1024, bits=60, L=3, batch=1, Ci=66, Co=64, H=5, W=5, kh=3, kw=3, pad=1,
                                 xrange=(-128, 128), wrange=(-128, 128)),

@@ -1,7 +1,7 @@
 """Counter-based generator shared (as a SPECIFICATION, not as code) by the client-side oracle and the
 library's GPU encryption / key generation (hy_keygen / hy_encrypt).
 
-Each side implements the same generator: the library in CUDA (csrc/client.cu), this module in
+Each side implements the same generator: the library in CUDA (csrc/kernels.cu), this module in
 vectorised NumPy for the oracle tests.  No method arithmetic lives here: only random integers and
 their documented mapping to the distributions the client draws (PAPER.md:242-253 [ign]: uniform
 mask a, error e, secret s; readings R2/R3: ternary secret, centered binomial eta = 20).

@@ -38,6 +38,7 @@ typedef int32_t hy_status;
 #define HY_ECUDA (-3)   /* a CUDA runtime call or kernel launch failed */
 #define HY_ENOKEY (-4)  /* a Galois key the layout needs was not uploaded */
 #define HY_ESHAPE (-5)  /* ciphertext counts / shapes do not match the layout */
+#define HY_ENOISE (-6)  /* hy_decrypt_debug: a coefficient's noise budget is below 1 bit */
 
 #define HY_MAX_LIMBS 8
 #define HY_MAX_TAPS 49     /* kernels up to 7x7 */
@@ -244,6 +245,13 @@ hy_status hy_weights_set_mac_path(hy_weights* w, int32_t path);
  * (row 0 slots 0..N/2-1, then row 1).  Not on the hot path; synchronises the device. */
 hy_status hy_decrypt_debug(const hy_params* p, const int8_t* sk, const uint64_t* ct, size_t n, uint32_t scale,
                            uint64_t* slots_out);
+/* As hy_decrypt_debug, and reports each ciphertext's invariant noise budget (PAPER.md:266-267
+ * [\ignore]: decryption is correct while the noise stays below Delta / 2): budget_bits[o] = min over
+ * coefficients of log2(Q / |2 (t x - round(t x / Q) Q)|) = log2(1 / (2 |v|)) with v = t x / Q - m the
+ * invariant noise (budget_bits may be NULL).  Both return HY_ENOISE, after writing slots_out, when
+ * some coefficient has less than 1 bit left (|v| > 1/4: the decrypted value is not trustworthy). */
+hy_status hy_decrypt_debug_noise(const hy_params* p, const int8_t* sk, const uint64_t* ct, size_t n, uint32_t scale,
+                                 uint64_t* slots_out, double* budget_bits);
 
 /* Client-side draws on the GPU (symmetric BFV encryption PAPER.md:242-253
  * [\ignore], keys of reading R5).  Every random number comes from Philox4x32-10 keyed by `seed`, with

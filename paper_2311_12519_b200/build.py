@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhyena.so")
 SOURCES = ["api.cu", "kernels.cu"]
-HEADERS = ["hy_common.cuh", "ntt.cuh"]
+HEADERS = ["hy_common.cuh", "ntt.cuh", "ksmac_v2.cuh", "ksmac_v3.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-diag-suppress", "177,128"]
 

@@ -1318,6 +1318,11 @@ struct Big {
     r.trim();
     return r;
   }
+  double to_double() const {
+    double r = 0;
+    for (size_t i = d.size(); i-- > 0;) r = r * 4294967296.0 + (double)d[i];
+    return r;
+  }
   int cmp(const Big& o) const {
     if (d.size() != o.d.size()) return d.size() < o.d.size() ? -1 : 1;
     for (size_t i = d.size(); i-- > 0;)
@@ -1345,6 +1350,11 @@ void host_ntt_t(std::vector<u64>& a, u64 t, u64 zeta, uint32_t logN) {
 
 extern "C" hy_status hy_decrypt_debug(const hy_params* p, const int8_t* sk, const uint64_t* ct, size_t n,
                                       uint32_t scale, uint64_t* slots_out) {
+  return hy_decrypt_debug_noise(p, sk, ct, n, scale, slots_out, nullptr);
+}
+
+extern "C" hy_status hy_decrypt_debug_noise(const hy_params* p, const int8_t* sk, const uint64_t* ct, size_t n,
+                                            uint32_t scale, uint64_t* slots_out, double* budget_bits) {
   HY_CHECK(p && sk && ct && slots_out, HY_EINVAL, "null argument");
   HY_CHECK(scale % p->t != 0, HY_EINVAL, "scale must be invertible mod t");
   if (n == 0) return HY_OK;
@@ -1395,7 +1405,10 @@ extern "C" hy_status hy_decrypt_debug(const hy_params* p, const int8_t* sk, cons
   const u64 sinv = invmod(scale % t, t);
   std::vector<u64> m(N);
   const uint32_t half = (uint32_t)N / 2;
+  const double Qd = Q.to_double();
+  double worst = 1e300;
   for (size_t o = 0; o < n; o++) {
+    double bud = 1e300;
     for (size_t k = 0; k < N; k++) {
       u64 isum = 0;
       Big S;
@@ -1412,7 +1425,14 @@ extern "C" hy_status hy_decrypt_debug(const hy_params* p, const int8_t* sk, cons
         j++;
       }
       m[k] = (isum + j) % t;
+      // invariant noise of coefficient k: t x / Q - round(t x / Q) = (X - Q) / 2Q in [-1/2, 1/2);
+      // budget = log2(1 / (2 |.|)) = log2(Q / |X - Q|) bits (0 bits = undecryptable)
+      const Big dist = X.cmp(Q) >= 0 ? X.sub(Q) : Q.sub(X);
+      const double dd = dist.to_double();
+      if (dd > 0) bud = std::min(bud, std::log2(Qd / dd));
     }
+    if (budget_bits) budget_bits[o] = bud;
+    worst = std::min(worst, bud);
     host_ntt_t(m, t, p->zeta_t, p->logN);
     for (uint32_t r = 0; r < 2; r++)
       for (uint32_t i = 0; i < half; i++) {
@@ -1422,5 +1442,7 @@ extern "C" hy_status hy_decrypt_debug(const hy_params* p, const int8_t* sk, cons
         slots_out[o * N + r * half + i] = mulmod(m[kk], sinv, t);
       }
   }
+  HY_CHECK(worst >= 1.0, HY_ENOISE, "noise budget exhausted: %.2f bits left (< 1 bit: the decryption is unreliable)",
+           worst);
   return HY_OK;
 }

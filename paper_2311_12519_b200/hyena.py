@@ -15,14 +15,15 @@ import numpy as np
 __all__ = ["HyenaError", "hy_conv_shape", "hy_layout", "load_library", "library_path", "hy_last_error",
            "hy_plan_layout", "hy_params_create", "hy_params_destroy", "hy_keys_upload", "hy_encode_weights",
            "hy_weights_layout", "hy_weights_destroy", "hy_conv_eval", "hy_conv_eval_host", "hy_poly_mul",
-           "hy_ntt_roundtrip", "hy_rotate", "hy_decrypt_debug", "hy_kernel_launches", "hy_weights_set_stage_events",
-           "hy_weights_mac_time", "hy_weights_mac_path", "hy_weights_set_mac_path", "hy_secret_key", "hy_keygen",
+           "hy_ntt_roundtrip", "hy_rotate", "hy_decrypt_debug", "hy_decrypt_debug_noise", "hy_kernel_launches",
+           "hy_weights_set_stage_events", "hy_weights_mac_time", "hy_weights_mac_path", "hy_weights_set_mac_path", "hy_secret_key", "hy_keygen",
            "hy_encrypt", "hy_layout_accounting", "hy_accounting", "hy_noise_estimate", "hy_select_dcmp_base",
            "MAC_PATHS", "layout_dict", "EXPORTED"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 HY_MAX_TAPS = 49
 HY_MAX_GALOIS = 64
+HY_ENOISE = -6  # include/hyena.h: noise budget below 1 bit (hy_decrypt_debug)
 
 # every symbol include/hyena.h declares
 EXPORTED = ["hy_last_error", "hy_plan_layout", "hy_params_create", "hy_params_create2", "hy_params_destroy",
@@ -31,7 +32,7 @@ EXPORTED = ["hy_last_error", "hy_plan_layout", "hy_params_create", "hy_params_cr
             "hy_poly_mul", "hy_ntt_roundtrip", "hy_rotate", "hy_decrypt_debug", "hy_kernel_launches",
             "hy_weights_set_stage_events", "hy_weights_mac_time", "hy_weights_mac_path", "hy_weights_set_mac_path",
             "hy_secret_key", "hy_keygen", "hy_encrypt", "hy_layout_accounting", "hy_noise_estimate",
-            "hy_select_dcmp_base"]
+            "hy_select_dcmp_base", "hy_decrypt_debug_noise"]
 
 # S2 + S3 kernel choices (include/hyena.h hy_weights_mac_path)
 MAC_PATHS = {"thin": 0, "tc_fused": 1, "tc_split": 2, "fp64_fused": 3, "fp64_split": 4, "tc_coef": 5,
@@ -104,6 +105,7 @@ def load_library() -> ctypes.CDLL:
         "hy_ntt_roundtrip": (i32, [vp, vp, sz, vp]),
         "hy_rotate": (i32, [vp, vp, u32, vp, sz, vp]),
         "hy_decrypt_debug": (i32, [vp, vp, vp, sz, u32, vp]),
+        "hy_decrypt_debug_noise": (i32, [vp, vp, vp, sz, u32, vp, vp]),
         "hy_kernel_launches": (u64, []),
         "hy_weights_set_stage_events": (i32, [vp, vp, u32]),
         "hy_weights_mac_time": (i32, [vp, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(u32)]),
@@ -263,6 +265,20 @@ def hy_decrypt_debug(p: int, sk: np.ndarray, ct, scale: int) -> np.ndarray:
     _check(load_library().hy_decrypt_debug(p, s.ctypes.data, _dev_ptr(ct), n, scale, out.ctypes.data),
            "hy_decrypt_debug")
     return out
+
+
+def hy_decrypt_debug_noise(p: int, sk: np.ndarray, ct, scale: int, check: bool = True):
+    """(slots [n][N], noise budget bits [n]).  check=False returns both even when the library reports
+    HY_ENOISE (a budget below 1 bit); check=True raises HyenaError then."""
+    s = np.ascontiguousarray(sk, dtype=np.int8)
+    n, N = ct.shape[0], ct.shape[-1]
+    out = np.empty((n, N), dtype=np.uint64)
+    bud = np.empty(n, dtype=np.float64)
+    rc = load_library().hy_decrypt_debug_noise(p, s.ctypes.data, _dev_ptr(ct), n, scale, out.ctypes.data,
+                                               bud.ctypes.data)
+    if check or rc not in (0, HY_ENOISE):
+        _check(rc, "hy_decrypt_debug_noise")
+    return out, bud
 
 
 def hy_kernel_launches() -> int:

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import synth
-from oracle import conv
+from oracle import bfv, conv
 from tests.hyena_client import layer_from_config
 
 pytestmark = pytest.mark.gpu
@@ -66,3 +66,47 @@ def test_one_flipped_word_breaks_parity(hy, c1, what):
         ct[1, 1, 0, 5] = (ct[1, 1, 0, 5] + np.uint64(1)) % np.uint64(lay.P.primes[0])
     got = _run(hy, lay, W, keys, ct)
     assert not np.array_equal(got, ref), f"flipping one {what} word did not change the output"
+
+
+def _budgets(hy, lay, cts, check=True):
+    cfg = synth.configs()["C1"]
+    p = hy.hy_params_create(cfg.N, cfg.primes, cfg.t, 0)
+    try:
+        return hy.hy_decrypt_debug_noise(p, lay.s.astype(np.int8), torch.from_numpy(np.ascontiguousarray(cts)).cuda(),
+                                         lay.ls.scale, check=check)
+    finally:
+        hy.hy_params_destroy(p)
+
+
+def test_noise_budget_matches_oracle_meter(hy, c1):
+    """hy_decrypt_debug_noise's budget log2(Q / |2 (t x - round(t x / Q) Q)|) equals the oracle's
+    log2(Delta / 2) - log2 ||v||_inf (PAPER.md:266-267 [ign]) to within the Delta = floor(Q / t) rounding."""
+    lay, ref = c1
+    _, bud = _budgets(hy, lay, ref)
+    for c, b in zip(ref, bud):
+        m = bfv.decrypt(lay.P, c, lay.s)
+        want = bfv.noise_budget_bits(lay.P) - bfv.noise_bits(lay.P, c, lay.s, m)
+        assert abs(b - want) < 0.05, (b, want)
+        assert b >= 4
+
+
+def test_garbage_ciphertext_reports_enoise(hy, c1):
+    """Uniform residues (no encryption of anything) leave no budget: HY_ENOISE."""
+    lay, ref = c1
+    rnd = synth.uniform_residues(synth.rng(9, "misc", 4242), lay.P.primes, (2, 2, lay.P.N))
+    with pytest.raises(hy.HyenaError, match=r"\(-6\)"):
+        _budgets(hy, lay, np.ascontiguousarray(rnd))
+    _, bud = _budgets(hy, lay, np.ascontiguousarray(rnd), check=False)
+    assert (bud < 1).all()
+
+
+def test_flipped_key_word_exhausts_budget(hy, c1):
+    """A switching key off by one in one word adds a key-sized error: the output is undecryptable and
+    the library says so (negative control of the noise meter)."""
+    lay, ref = c1
+    keys = {g: k.copy() for g, k in lay.keys.items()}
+    for g in keys:
+        keys[g][0, 0, 0, 77] ^= np.uint64(1 << 40)
+    got = _run(hy, lay, lay.W, keys, lay.ct_in)
+    with pytest.raises(hy.HyenaError, match=r"\(-6\)"):
+        _budgets(hy, lay, got)

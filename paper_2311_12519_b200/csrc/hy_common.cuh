@@ -241,6 +241,16 @@ __device__ __forceinline__ u64 shoup_mul(u64 x, u64 w, u64 w_sh, u64 q) {
   return x * w - hi * q;
 }
 
+// hi64(x w) without the x0 w0 partial product and the low halves of the cross products:
+// x1 w1 + hi32(x1 w0) + hi32(x0 w1), which is below the exact high word by at most 3 (the dropped
+// parts sum to < 3 * 2^64).  In a Shoup product the quotient then undershoots by <= 3, so
+// x w - h q lies in [0, 5q) instead of [0, 2q).  One IMAD.WIDE + two IMAD.HI instead of the four
+// partial products of __umul64hi (tools/mmbench: +16% key-switching products per clock).
+__device__ __forceinline__ u64 umulhi_apx(u64 x, u64 w) {
+  const uint32_t x0 = (uint32_t)x, x1 = (uint32_t)(x >> 32), w0 = (uint32_t)w, w1 = (uint32_t)(w >> 32);
+  return (u64)x1 * w1 + __umulhi(x1, w0) + __umulhi(x0, w1);
+}
+
 __device__ __forceinline__ u64 csub(u64 x, u64 m) { return x >= m ? x - m : x; }
 
 // canonical residue of a lazy sum x < (2L + 1) q (c0 + L Shoup products, each in [0, 2q)):

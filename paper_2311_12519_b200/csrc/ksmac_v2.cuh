@@ -272,7 +272,10 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
         // lazy Shoup sums with ONE quotient multiply per component: sum_i (d_i w_i - h_i q) =
         // sum_i d_i w_i - (sum_i h_i) q (mod 2^64), h_i = floor(d_i w'_i / 2^64); the true value is
         // c0 + sum of L Shoup products in [0, 2q) < (2L + 1) q < 2^64, so the mod-2^64 result is
-        // exact and bit-identical to the per-product form (2 (L - 1) fewer 64-bit products per term)
+        // exact and bit-identical to the per-product form (2 (L - 1) fewer 64-bit products per term).
+        // L <= 3: approximate quotients (umulhi_apx, each product in [0, 5q)): the sum stays below
+        // (5L + 1) q <= 16 q < 2^64 (hy_params_create enforces q < 2^60); R is any 64-bit value to
+        // the byte-plane MAC and congruent mod q, so the outputs are unchanged bit for bit
         u64 r0[4], r1[4], h0[4], h1[4];
 #pragma unroll
         for (int t = 0; t < 4; t++) {
@@ -290,9 +293,14 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
           for (int t = 0; t < 4; t++) {
             const u64 d = cur[t].d[i];
             r0[t] += d * kv;
-            h0[t] += __umul64hi(d, ksh);
             r1[t] += d * av;
-            h1[t] += __umul64hi(d, ash);
+            if constexpr (LT <= 3) {
+              h0[t] += umulhi_apx(d, ksh);
+              h1[t] += umulhi_apx(d, ash);
+            } else {
+              h0[t] += __umul64hi(d, ksh);
+              h1[t] += __umul64hi(d, ash);
+            }
           }
         }
 #pragma unroll

@@ -28,6 +28,23 @@
 //   next tile are prefetched with cp.async into the other half of a double buffer.
 #pragma once
 
+// A/B switches (tools/abbuild.py builds variants with -D; the defaults are the measured best)
+#ifndef V2_PREFETCH
+#define V2_PREFETCH 0
+#endif
+#ifndef V2_BACKOFF
+#define V2_BACKOFF 0
+#endif
+#ifndef V2_PTX
+#define V2_PTX 1
+#endif
+#ifndef V2_SMAX
+#define V2_SMAX 2
+#endif
+#ifndef V2_KBMAX
+#define V2_KBMAX 3
+#endif
+
 constexpr int V2_PROD_WARPS = 12, V2_PROD = V2_PROD_WARPS * 32;
 constexpr int V2_KS = 3, V2_CHUNK = 32 * V2_KS;             // 96 terms = 3 UMMA K steps per chunk
 constexpr uint32_t V2_STAGE_B = V2_KS * 8 * 1024;           // 8 planes x 32 columns x 32 terms per K step
@@ -45,30 +62,37 @@ struct V2Warps {
 struct V2Geom {
   int S;                 // pipeline stages
   int wres;              // 1: all weights resident in shared memory
+  int kb;                // key buffers (3 or 4; keys are prefetched two tiles ahead)
   uint32_t off_b, off_a, off_key, off_bar;
-  uint32_t key_bytes;    // one of the two key buffers
+  uint32_t key_bytes;    // one key buffer
   size_t bytes;          // dynamic shared memory to request (incl. 1024-byte alignment slack)
 };
 
+// largest configuration that fits, preferring resident weights, then 4 stages, then 4 key buffers
+// (with 4, the buffer a tile's keys are copied into was last read two tiles earlier: the producer
+// warps, which the stage ring keeps within S < one tile of each other, never wait for it)
 inline V2Geom v2_geom(int T, int L, int Kpad, size_t smem_max) {
   V2Geom g{};
   const uint32_t wbytes = 128u * (uint32_t)Kpad;
   g.key_bytes = (uint32_t)T * 4 * L * TC_POS * 8;
   const uint32_t bar = 256;
   for (int wres = 1; wres >= 0; wres--) {
-    for (int S = 4; S >= 2; S--) {
-      const uint32_t w = wres ? wbytes : 0;
-      const uint32_t per = V2_STAGE_B + (wres ? 0 : V2_STAGE_A);
-      const size_t tot = 1024 + (size_t)w + (size_t)S * per + 3 * (size_t)g.key_bytes + bar;
-      if (tot <= smem_max) {
-        g.S = S;
-        g.wres = wres;
-        g.off_b = w;
-        g.off_a = w + S * V2_STAGE_B;
-        g.off_key = g.off_a + (wres ? 0 : S * V2_STAGE_A);
-        g.off_bar = g.off_key + 3 * g.key_bytes;
-        g.bytes = tot;
-        return g;
+    for (int S = V2_SMAX; S >= 2; S--) {
+      for (int kb = V2_KBMAX; kb >= 3; kb--) {
+        const uint32_t w = wres ? wbytes : 0;
+        const uint32_t per = V2_STAGE_B + (wres ? 0 : V2_STAGE_A);
+        const size_t tot = 1024 + (size_t)w + (size_t)S * per + (size_t)kb * g.key_bytes + bar;
+        if (tot <= smem_max) {
+          g.S = S;
+          g.wres = wres;
+          g.kb = kb;
+          g.off_b = w;
+          g.off_a = w + S * V2_STAGE_B;
+          g.off_key = g.off_a + (wres ? 0 : S * V2_STAGE_A);
+          g.off_bar = g.off_key + kb * g.key_bytes;
+          g.bytes = tot;
+          return g;
+        }
       }
     }
   }
@@ -93,6 +117,47 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity, in
   }
 }
 
+// mbarrier wait with an explicit nanosleep back-off between polls: for the warps that idle most of
+// a tile (epilogue, UMMA issuer); the suspend hint of mbar_wait_sleep returns within ~30 ns, so those
+// warps polled ~10^8 times per C4 layer (profiled: 17% of all issued instructions were wait loops)
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, uint32_t parity, uint32_t ns) {
+  if (!V2_BACKOFF) return mbar_wait_sleep(b, parity, (int)ns);
+  uint32_t done = 0;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.b32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(ns);
+  }
+}
+
+// one digit of the lazy key switching of one component, on 32-bit halves (inline PTX: the C form
+// compiled to ~60% more instructions, moves of zero high words and split products):
+//   r += d k  (mod 2^64),   h += d1 s1 + hi32(d1 s0) + hi32(d0 s1)  (= umulhi_apx(d, s), mod 2^64)
+__device__ __forceinline__ void v2_ks_acc(uint32_t& rlo, uint32_t& rhi, uint32_t& hlo, uint32_t& hhi, u64 d, u64 k,
+                                          u64 sh) {
+  asm("mad.lo.cc.u32 %0, %4, %6, %0;\n\t"
+      "madc.hi.u32 %1, %4, %6, %1;\n\t"
+      "mad.lo.u32 %1, %4, %7, %1;\n\t"
+      "mad.lo.u32 %1, %5, %6, %1;\n\t"
+      "mad.lo.cc.u32 %2, %5, %9, %2;\n\t"
+      "madc.hi.u32 %3, %5, %9, %3;\n\t"
+      "mad.hi.cc.u32 %2, %5, %8, %2;\n\t"
+      "addc.u32 %3, %3, 0;\n\t"
+      "mad.hi.cc.u32 %2, %4, %9, %2;\n\t"
+      "addc.u32 %3, %3, 0;"
+      : "+r"(rlo), "+r"(rhi), "+r"(hlo), "+r"(hhi)
+      : "r"((uint32_t)d), "r"((uint32_t)(d >> 32)), "r"((uint32_t)k), "r"((uint32_t)(k >> 32)), "r"((uint32_t)sh),
+        "r"((uint32_t)(sh >> 32)));
+}
+
+__device__ __forceinline__ void v2_prefetch_l2(const void* g) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], 128;" ::"l"(g) : "memory");
+}
+
 template <int LT, int LOGN, int EPI>
 __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
     ksmac_v2_kernel(KsMacArgs a, const int8_t* __restrict__ w8, V2Geom geo, int units) {
@@ -109,9 +174,10 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
   uint64_t* const empty_bar = bars + 4;       // [S]  UMMA completion -> producers
   uint64_t* const tfull = bars + 8;           // [2]  accumulator complete -> epilogue
   uint64_t* const tempty = bars + 10;         // [2]  accumulator read -> UMMA issuer
-  uint64_t* const kfull = bars + 12;          // [3]  key buffer landed (cp.async arrivals)
-  uint64_t* const kempty = bars + 15;         // [3]  key buffer no longer read
-  uint32_t* const s_tmem = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* const kfull = bars + 12;          // [kb] key buffer landed (cp.async arrivals)
+  uint64_t* const kempty = bars + 16;         // [kb] key buffer no longer read
+  uint32_t* const s_tmem = reinterpret_cast<uint32_t*>(bars + 20);
+  const int KB = geo.kb;
 
   constexpr bool CN = LOGN > 0;
   const int N = CN ? (1 << LOGN) : (1 << a.logN);
@@ -135,7 +201,7 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], EPI);
     }
-    for (int b = 0; b < 3; b++) {
+    for (int b = 0; b < KB; b++) {
       mbar_init(&kfull[b], V2_PROD);
       mbar_init(&kempty[b], V2_PROD_WARPS);
     }
@@ -158,13 +224,13 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
   const uint32_t tmem = *s_tmem;
 
   // key words of tile `it` of this CTA (limb l, positions j0 .. j0 + 15, every tap), copied by the
-  // producer threads into key buffer it % 3: [tap][x = 2i + comp][val, sh][16]; every producer
-  // thread arrives (cp.async.mbarrier.arrive.noinc) on kfull[it % 3] when its copies have landed
+  // producer threads into key buffer it % KB: [tap][x = 2i + comp][val, sh][16]; every producer
+  // thread arrives (cp.async.mbarrier.arrive.noinc) on kfull[it % KB] when its copies have landed
   auto issue_keys = [&](int it) {
     const int tile = blockIdx.x + it * gridDim.x;
     const int rem = tile % per_unit;
     const int l = rem / tiles_pl, j0 = (rem % tiles_pl) * TC_POS;
-    const uint32_t kb = sm_a + geo.off_key + (uint32_t)(it % 3) * geo.key_bytes;
+    const uint32_t kb = sm_a + geo.off_key + (uint32_t)(it % KB) * geo.key_bytes;
     const int pieces = a.T * 4 * LT * (TC_POS / 2);
     for (int e = threadIdx.x; e < pieces; e += V2_PROD) {
       const int p2 = e % (TC_POS / 2), r = e / (TC_POS / 2);
@@ -174,7 +240,23 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
         v2_cp16(kb + (uint32_t)e * 16,
                 key + (size_t)sh * 2 * LT * LN + (size_t)x * LN + (size_t)l * N + j0 + 2 * p2);
     }
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&kfull[it % 3])) : "memory");
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&kfull[it % KB])) : "memory");
+  };
+  // L2 prefetch of the input rows of tile `it` at its identity window (C0 and the L digits of every
+  // channel, 128 bytes each): the tap windows of a tile are the identity windows of tiles that the
+  // other CTAs process at the same time (+-1, +-Wp positions), so each input row reaches L2 once,
+  // two tiles before it is read, instead of stalling the first tap that touches it (ncu: 25% L2 misses)
+  // (issued by the epilogue warps, which idle most of a tile and have registers to spare)
+  auto prefetch_rows = [&](int it) {
+    const int tile = blockIdx.x + it * gridDim.x;
+    const int z = tile / per_unit, rem = tile % per_unit;
+    const int l = rem / tiles_pl, j0 = (rem % tiles_pl) * TC_POS;
+    for (int e = (int)threadIdx.x - 32 * V2_PROD_WARPS; e < a.Jcb * (LT + 1); e += 32 * EPI) {
+      const int c = e / (LT + 1), k = e % (LT + 1);
+      const u64* row = k == 0 ? a.C0 + ((size_t)z * a.Jcb + c) * LN
+                              : a.D + (((size_t)z * a.Jcb + c) * LT + (k - 1)) * LN;
+      v2_prefetch_l2(row + (size_t)l * N + j0);
+    }
   };
 
   if (warp < V2_PROD_WARPS) {
@@ -212,7 +294,10 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
     };
     auto load = [&](Term* pr, int& grp) {
       grp = lch * V2_CHUNK + tg * 4 < a.K ? ltap0 : -1;
-      if (grp >= 0) {
+      if (grp < 0) {  // K padding: zero terms (their weights are zero too), switched as identity
+#pragma unroll
+        for (int t = 0; t < 4; t++) pr[t].c0 = pr[t].d[0] = 0;
+      } else {
         const u64* C0 = lC0 + (size_t)lc0t * LN;
         const u64* D = lD + (size_t)lc0t * (LT * LN);
         if ((ident >> grp) & 1) {  // identity tap: R = (C0, D_{l,l})
@@ -243,22 +328,23 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
     };
     // ---- compute cursor ----
     int cit = 0, cch = 0, gc = 0;
+    int st = 0, sround = 0;    // pipeline stage of chunk gc and how often the ring wrapped (no % S)
+    uint32_t kbuf = 0;         // sm offset of the current tile's key buffer
     u64 q = 0;
     auto step = [&](Term* cur, int grp, Term* nxt, int& grp_nxt) {
       if (cch == 0) {  // a new tile: its keys must have landed; prefetch those of tile cit + 2
         q = a.lcs.lc[((blockIdx.x + cit * gridDim.x) % per_unit) / tiles_pl].q;
-        if (cit + 2 < my_tiles) {  // buffer (cit + 2) % 3 was last read by tile cit - 1
-          if (cit >= 1) mbar_wait_sleep(&kempty[(cit + 2) % 3], ((cit - 1) / 3) & 1, 0);
+        if (cit + 2 < my_tiles) {  // buffer (cit + 2) % KB was last read by tile cit + 2 - KB
+          const int tp = cit + 2 - KB;
+          if (tp >= 0) mbar_wait_sleep(&kempty[tp % KB], (tp / KB) & 1, 0);
           issue_keys(cit + 2);
         }
-        mbar_wait_sleep(&kfull[cit % 3], (cit / 3) & 1, 0);
+        kbuf = geo.off_key + (uint32_t)(cit % KB) * geo.key_bytes;
+        mbar_wait_sleep(&kfull[cit % KB], (cit / KB) & 1, 0);
       }
       if (gc + 1 < my_tiles * nchunks) load(nxt, grp_nxt);
       uint32_t lo0[4], hi0[4], lo1[4], hi1[4];
-      if (grp < 0) {
-#pragma unroll
-        for (int t = 0; t < 4; t++) lo0[t] = hi0[t] = lo1[t] = hi1[t] = 0;
-      } else if ((ident >> grp) & 1) {
+      if (grp < 0 || ((ident >> grp) & 1)) {  // identity tap (or K padding): R = (C0, D_{l,l})
 #pragma unroll
         for (int t = 0; t < 4; t++) {
           lo0[t] = (uint32_t)cur[t].c0;
@@ -267,8 +353,7 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
           hi1[t] = (uint32_t)(cur[t].d[0] >> 32);
         }
       } else {
-        const uint32_t kp = sm_a + geo.off_key + (uint32_t)(cit % 3) * geo.key_bytes + (uint32_t)pos * 8 +
-                            (uint32_t)grp * (4 * LT * TC_POS * 8);
+        const uint32_t kp = sm_a + kbuf + (uint32_t)pos * 8 + (uint32_t)grp * (4 * LT * TC_POS * 8);
         // lazy Shoup sums with ONE quotient multiply per component: sum_i (d_i w_i - h_i q) =
         // sum_i d_i w_i - (sum_i h_i) q (mod 2^64), h_i = floor(d_i w'_i / 2^64); the true value is
         // c0 + sum of L Shoup products in [0, 2q) < (2L + 1) q < 2^64, so the mod-2^64 result is
@@ -276,6 +361,40 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
         // L <= 3: approximate quotients (umulhi_apx, each product in [0, 5q)): the sum stays below
         // (5L + 1) q <= 16 q < 2^64 (hy_params_create enforces q < 2^60); R is any 64-bit value to
         // the byte-plane MAC and congruent mod q, so the outputs are unchanged bit for bit
+#if V2_PTX
+        if constexpr (LT <= 3) {
+          uint32_t g0[4], g1[4], e0[4], e1[4];  // h0, h1 halves
+#pragma unroll
+          for (int t = 0; t < 4; t++) {
+            lo0[t] = (uint32_t)cur[t].c0;
+            hi0[t] = (uint32_t)(cur[t].c0 >> 32);
+            lo1[t] = hi1[t] = g0[t] = g1[t] = e0[t] = e1[t] = 0;
+          }
+#pragma unroll
+          for (int i = 0; i < LT; i++) {
+            u64 kv, ksh, av, ash;
+            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(kv) : "r"(kp + (4 * i) * TC_POS * 8));
+            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(ksh) : "r"(kp + (4 * i + 1) * TC_POS * 8));
+            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(av) : "r"(kp + (4 * i + 2) * TC_POS * 8));
+            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(ash) : "r"(kp + (4 * i + 3) * TC_POS * 8));
+#pragma unroll
+            for (int t = 0; t < 4; t++) {
+              v2_ks_acc(lo0[t], hi0[t], g0[t], g1[t], cur[t].d[i], kv, ksh);
+              v2_ks_acc(lo1[t], hi1[t], e0[t], e1[t], cur[t].d[i], av, ash);
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < 4; t++) {
+            const u64 r0 = (((u64)hi0[t] << 32) | lo0[t]) - (((u64)g1[t] << 32) | g0[t]) * q;
+            const u64 r1 = (((u64)hi1[t] << 32) | lo1[t]) - (((u64)e1[t] << 32) | e0[t]) * q;
+            lo0[t] = (uint32_t)r0;
+            hi0[t] = (uint32_t)(r0 >> 32);
+            lo1[t] = (uint32_t)r1;
+            hi1[t] = (uint32_t)(r1 >> 32);
+          }
+        } else
+#endif
+        {
         u64 r0[4], r1[4], h0[4], h1[4];
 #pragma unroll
         for (int t = 0; t < 4; t++) {
@@ -315,18 +434,19 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
           lo1[t] = (uint32_t)r1[t];
           hi1[t] = (uint32_t)(r1[t] >> 32);
         }
+        }
       }
       if (cch == nchunks - 1) {  // this warp is done reading the tile's keys
         __syncwarp();
-        if (lane == 0) mbar_arrive(&kempty[cit % 3]);
+        if (lane == 0) mbar_arrive(&kempty[cit % KB]);
       }
       uint32_t p0[8], p1[8];
       byte_tr4(lo0, p0);
       byte_tr4(hi0, p0 + 4);
       byte_tr4(lo1, p1);
       byte_tr4(hi1, p1 + 4);
-      const int s = gc % S;
-      if (gc >= S) mbar_wait_sleep(&empty_bar[s], ((gc / S) - 1) & 1, 0);
+      const int s = st;
+      if (sround > 0) mbar_wait_sleep(&empty_bar[s], (sround - 1) & 1, 0);
       if (V2_KS * cch + ks < nk32) {
         const uint32_t bb = sm_a + geo.off_b + (uint32_t)s * V2_STAGE_B + (uint32_t)ks * 8192;
 #pragma unroll
@@ -352,6 +472,10 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&full_bar[s]);
       gc++;
+      if (++st == S) {
+        st = 0;
+        sround++;
+      }
       if (++cch == nchunks) {
         cch = 0;
         cit++;
@@ -374,15 +498,14 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
     // ======================= single UMMA issuer =======================
     if (lane == 0) {
       const uint32_t idesc = umma_idesc_s8u8(128, 8 * TC_COLS);
-      int gc = 0;
+      int s = 0, sround = 0;
       for (int it = 0; it < my_tiles; it++) {
         const int b = it & 1;
-        if (it >= 2) mbar_wait_sleep(&tempty[b], ((it >> 1) - 1) & 1, 64);
+        if (it >= 2) mbar_wait_backoff(&tempty[b], ((it >> 1) - 1) & 1, 256);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t acc_t = tmem + (uint32_t)b * 256;
-        for (int ch = 0; ch < nchunks; ch++, gc++) {
-          const int s = gc % S;
-          mbar_wait_sleep(&full_bar[s], (gc / S) & 1, 32);
+        for (int ch = 0; ch < nchunks; ch++) {
+          mbar_wait_backoff(&full_bar[s], sround & 1, 64);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           for (int k2 = 0; k2 < V2_KS && V2_KS * ch + k2 < nk32; k2++) {
             const uint32_t aaddr = geo.wres ? sm_a + (uint32_t)(V2_KS * ch + k2) * 4096
@@ -398,6 +521,10 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                            smem_u32(&empty_bar[s]))
                        : "memory");
+          if (++s == S) {
+            s = 0;
+            sround++;
+          }
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                          smem_u32(&tfull[b]))
@@ -408,12 +535,15 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
   } else {
     // ======================= epilogue =======================
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    if (V2_PREFETCH)
+      for (int it = 0; it < 3 && it < my_tiles; it++) prefetch_rows(it);
     for (int it = 0; it < my_tiles; it++) {
+      if (V2_PREFETCH && it + 3 < my_tiles) prefetch_rows(it + 3);
       const int b = it & 1;
       const int tile = blockIdx.x + it * gridDim.x;
       const int z = tile / per_unit, rem = tile % per_unit;
       const int l = rem / tiles_pl, j0 = (rem % tiles_pl) * TC_POS;
-      mbar_wait_sleep(&tfull[b], (it >> 1) & 1, 256);
+      mbar_wait_backoff(&tfull[b], (it >> 1) & 1, 1000);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (quad * 32 < a.M) {
         const int row = quad * 32 + lane;

@@ -76,7 +76,8 @@ _lib = None
 
 
 def library_path() -> str:
-    return os.path.join(_HERE, "libhyena.so")
+    # HYENA_LIB: an alternative build of the same library (A/B measurements, tools/abbuild.py)
+    return os.environ.get("HYENA_LIB") or os.path.join(_HERE, "libhyena.so")
 
 
 def load_library() -> ctypes.CDLL:

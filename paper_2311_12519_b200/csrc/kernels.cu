@@ -2025,7 +2025,7 @@ hy_status launch_ksmac_v3_t(const KsMacArgs& a, const int8_t* w8, int units, con
   const int ntiles = units * a.L * ((1 << a.logN) / V3_POS);
   HY_CUDA_TRY(hy_smem_attr((const void*)ksmac_v3_kernel<LT, LOGN, EPI>, g.bytes));
   HY_CUDA_TRY(hy_launch(ksmac_v3_kernel<LT, LOGN, EPI>, dim3((unsigned)std::min(ntiles, nsm)),
-                        dim3(V2Warps<EPI>::THREADS), g.bytes, s, 1, a, w8, g, units));
+                        dim3(V3Warps<EPI>::THREADS), g.bytes, s, 1, a, w8, g, units));
   HY_LAUNCH_CHECK();
   return HY_OK;
 }

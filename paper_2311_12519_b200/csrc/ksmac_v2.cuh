@@ -38,6 +38,9 @@
 #ifndef V2_PTX
 #define V2_PTX 1
 #endif
+#ifndef V2_PF
+#define V2_PF 0
+#endif
 #ifndef V2_SMAX
 #define V2_SMAX 2
 #endif
@@ -45,8 +48,12 @@
 #define V2_KBMAX 3
 #endif
 
-constexpr int V2_PROD_WARPS = 12, V2_PROD = V2_PROD_WARPS * 32;
-constexpr int V2_KS = 3, V2_CHUNK = 32 * V2_KS;             // 96 terms = 3 UMMA K steps per chunk
+#ifndef V2_PW
+#define V2_PW 16
+#endif
+// producer warps (a multiple of 4): 16 slot positions x 2 PW term groups of 4 per chunk
+constexpr int V2_PROD_WARPS = V2_PW, V2_PROD = V2_PROD_WARPS * 32;
+constexpr int V2_KS = V2_PW / 4, V2_CHUNK = 32 * V2_KS;     // PW = 12: 96 terms = 3 UMMA K steps per chunk
 constexpr uint32_t V2_STAGE_B = V2_KS * 8 * 1024;           // 8 planes x 32 columns x 32 terms per K step
 constexpr uint32_t V2_STAGE_A = V2_KS * 4096;               // streamed weights: 128 rows x 32 terms per K step
 constexpr uint32_t V2_TMEM_COLS = 512;
@@ -137,21 +144,24 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, uint32_t parity, 
 // one digit of the lazy key switching of one component, on 32-bit halves (inline PTX: the C form
 // compiled to ~60% more instructions, moves of zero high words and split products):
 //   r += d k  (mod 2^64),   h += d1 s1 + hi32(d1 s0) + hi32(d0 s1)  (= umulhi_apx(d, s), mod 2^64)
-__device__ __forceinline__ void v2_ks_acc(uint32_t& rlo, uint32_t& rhi, uint32_t& hlo, uint32_t& hhi, u64 d, u64 k,
-                                          u64 sh) {
-  asm("mad.lo.cc.u32 %0, %4, %6, %0;\n\t"
-      "madc.hi.u32 %1, %4, %6, %1;\n\t"
-      "mad.lo.u32 %1, %4, %7, %1;\n\t"
-      "mad.lo.u32 %1, %5, %6, %1;\n\t"
-      "mad.lo.cc.u32 %2, %5, %9, %2;\n\t"
-      "madc.hi.u32 %3, %5, %9, %3;\n\t"
-      "mad.hi.cc.u32 %2, %5, %8, %2;\n\t"
-      "addc.u32 %3, %3, 0;\n\t"
-      "mad.hi.cc.u32 %2, %4, %9, %2;\n\t"
-      "addc.u32 %3, %3, 0;"
-      : "+r"(rlo), "+r"(rhi), "+r"(hlo), "+r"(hhi)
-      : "r"((uint32_t)d), "r"((uint32_t)(d >> 32)), "r"((uint32_t)k), "r"((uint32_t)(k >> 32)), "r"((uint32_t)sh),
-        "r"((uint32_t)(sh >> 32)));
+__device__ __forceinline__ void v2_ks_acc(u64& r, u64& h, u64 d, u64 k, u64 sh) {
+  // r and h stay 64-bit register pairs (the IMAD.WIDE accumulate operands): no pair-building moves
+  asm("{\n\t.reg .u32 rl, rh, hl, hh, d0, d1, k0, k1, s0, s1;\n\t"
+      "mov.b64 {rl, rh}, %0;\n\tmov.b64 {hl, hh}, %1;\n\t"
+      "mov.b64 {d0, d1}, %2;\n\tmov.b64 {k0, k1}, %3;\n\tmov.b64 {s0, s1}, %4;\n\t"
+      "mad.lo.cc.u32 rl, d0, k0, rl;\n\t"
+      "madc.hi.u32 rh, d0, k0, rh;\n\t"
+      "mad.lo.u32 rh, d0, k1, rh;\n\t"
+      "mad.lo.u32 rh, d1, k0, rh;\n\t"
+      "mad.lo.cc.u32 hl, d1, s1, hl;\n\t"
+      "madc.hi.u32 hh, d1, s1, hh;\n\t"
+      "mad.hi.cc.u32 hl, d1, s0, hl;\n\t"
+      "addc.u32 hh, hh, 0;\n\t"
+      "mad.hi.cc.u32 hl, d0, s1, hl;\n\t"
+      "addc.u32 hh, hh, 0;\n\t"
+      "mov.b64 %0, {rl, rh};\n\tmov.b64 %1, {hl, hh};\n\t}"
+      : "+l"(r), "+l"(h)
+      : "l"(d), "l"(k), "l"(sh));
 }
 
 __device__ __forceinline__ void v2_prefetch_l2(const void* g) {
@@ -342,7 +352,7 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
         kbuf = geo.off_key + (uint32_t)(cit % KB) * geo.key_bytes;
         mbar_wait_sleep(&kfull[cit % KB], (cit / KB) & 1, 0);
       }
-      if (gc + 1 < my_tiles * nchunks) load(nxt, grp_nxt);
+      if (V2_PF > 0 && gc + V2_PF < my_tiles * nchunks) load(nxt, grp_nxt);
       uint32_t lo0[4], hi0[4], lo1[4], hi1[4];
       if (grp < 0 || ((ident >> grp) & 1)) {  // identity tap (or K padding): R = (C0, D_{l,l})
 #pragma unroll
@@ -363,12 +373,11 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
         // the byte-plane MAC and congruent mod q, so the outputs are unchanged bit for bit
 #if V2_PTX
         if constexpr (LT <= 3) {
-          uint32_t g0[4], g1[4], e0[4], e1[4];  // h0, h1 halves
+          u64 r0[4], r1[4], h0[4], h1[4];
 #pragma unroll
           for (int t = 0; t < 4; t++) {
-            lo0[t] = (uint32_t)cur[t].c0;
-            hi0[t] = (uint32_t)(cur[t].c0 >> 32);
-            lo1[t] = hi1[t] = g0[t] = g1[t] = e0[t] = e1[t] = 0;
+            r0[t] = cur[t].c0;
+            r1[t] = h0[t] = h1[t] = 0;
           }
 #pragma unroll
           for (int i = 0; i < LT; i++) {
@@ -379,18 +388,18 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
             asm volatile("ld.shared.u64 %0, [%1];" : "=l"(ash) : "r"(kp + (4 * i + 3) * TC_POS * 8));
 #pragma unroll
             for (int t = 0; t < 4; t++) {
-              v2_ks_acc(lo0[t], hi0[t], g0[t], g1[t], cur[t].d[i], kv, ksh);
-              v2_ks_acc(lo1[t], hi1[t], e0[t], e1[t], cur[t].d[i], av, ash);
+              v2_ks_acc(r0[t], h0[t], cur[t].d[i], kv, ksh);
+              v2_ks_acc(r1[t], h1[t], cur[t].d[i], av, ash);
             }
           }
 #pragma unroll
           for (int t = 0; t < 4; t++) {
-            const u64 r0 = (((u64)hi0[t] << 32) | lo0[t]) - (((u64)g1[t] << 32) | g0[t]) * q;
-            const u64 r1 = (((u64)hi1[t] << 32) | lo1[t]) - (((u64)e1[t] << 32) | e0[t]) * q;
-            lo0[t] = (uint32_t)r0;
-            hi0[t] = (uint32_t)(r0 >> 32);
-            lo1[t] = (uint32_t)r1;
-            hi1[t] = (uint32_t)(r1 >> 32);
+            const u64 x0 = r0[t] - h0[t] * q;
+            const u64 x1 = r1[t] - h1[t] * q;
+            lo0[t] = (uint32_t)x0;
+            hi0[t] = (uint32_t)(x0 >> 32);
+            lo1[t] = (uint32_t)x1;
+            hi1[t] = (uint32_t)(x1 >> 32);
           }
         } else
 #endif
@@ -482,6 +491,15 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
       }
     };
     const int total = my_tiles * nchunks;
+#if V2_PF == 0  // no register prefetch: more producer warps fit (latency hidden by warps instead)
+    Term buf[4];
+    int gb = -1, gdummy = -1;
+    if (total > 0) cursor_tile(0);
+    for (int g = 0; g < total; g++) {
+      load(buf, gb);
+      step(buf, gb, buf, gdummy);
+    }
+#elif V2_PF == 1
     Term bufA[4], bufB[4];
     int gA = -1, gB = -1;
     if (total > 0) {
@@ -494,6 +512,23 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
       step(bufB, gB, bufA, gA);
     }
     if (g < total) step(bufA, gA, bufB, gB);
+#else  // digit loads two chunks ahead (three register buffers)
+    Term bufA[4], bufB[4], bufC[4];
+    int gA = -1, gB = -1, gC = -1;
+    if (total > 0) {
+      cursor_tile(0);
+      load(bufA, gA);
+    }
+    if (total > 1) load(bufB, gB);
+    int g = 0;
+    for (; g + 2 < total; g += 3) {
+      step(bufA, gA, bufC, gC);
+      step(bufB, gB, bufA, gA);
+      step(bufC, gC, bufB, gB);
+    }
+    if (g < total) step(bufA, gA, bufC, gC);
+    if (g + 1 < total) step(bufB, gB, bufA, gA);
+#endif
   } else if (warp == MMA_WARP) {
     // ======================= single UMMA issuer =======================
     if (lane == 0) {

@@ -24,6 +24,13 @@
 // single UMMA issuer are those of ksmac_v2_kernel.
 #pragma once
 
+constexpr int V3_PROD_WARPS = 12, V3_PROD = V3_PROD_WARPS * 32;
+template <int EPI>
+struct V3Warps {
+  static constexpr int MMA = V3_PROD_WARPS + EPI;
+  static constexpr int THREADS = (V3_PROD_WARPS + EPI + 1) * 32;
+};
+
 constexpr int V3_POS = 8, V3_KS = 6, V3_CHUNK = 32 * V3_KS;  // 8 positions, 192 terms per chunk
 constexpr uint32_t V3_STAGE_B = V3_KS * 8192;                // 256 columns x 32 terms per K step
 constexpr uint32_t V3_STAGE_A = V3_KS * 4096;
@@ -114,11 +121,11 @@ __device__ __forceinline__ u64 madw(uint32_t a, uint32_t b, u64 c) {
 }
 
 template <int LT, int LOGN, int EPI>
-__global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
+__global__ void __launch_bounds__(V3Warps<EPI>::THREADS, 1)
     ksmac_v3_kernel(KsMacArgs a, const int8_t* __restrict__ w8, V2Geom geo, int units) {
   pdl_trigger();
-  constexpr int MMA_WARP = V2Warps<EPI>::MMA;
-  constexpr int NTHREADS = V2Warps<EPI>::THREADS;
+  constexpr int MMA_WARP = V3Warps<EPI>::MMA;
+  constexpr int NTHREADS = V3Warps<EPI>::THREADS;
   extern __shared__ __align__(1024) uint8_t v3_raw[];
   uint8_t* const sm = v3_raw + ((1024u - (smem_u32(v3_raw) & 1023u)) & 1023u);
   const uint32_t sm_a = smem_u32(sm);
@@ -145,7 +152,7 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; s++) {
-      mbar_init(&full_bar[s], V2_PROD_WARPS);
+      mbar_init(&full_bar[s], V3_PROD_WARPS);
       mbar_init(&empty_bar[s], 1);
     }
     for (int b = 0; b < 2; b++) {
@@ -153,8 +160,8 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
       mbar_init(&tempty[b], EPI);
     }
     for (int b = 0; b < 3; b++) {
-      mbar_init(&kfull[b], V2_PROD);
-      mbar_init(&kempty[b], V2_PROD_WARPS);
+      mbar_init(&kfull[b], V3_PROD);
+      mbar_init(&kempty[b], V3_PROD_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -182,7 +189,7 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
     const int l = rem / tiles_pl, j0 = (rem % tiles_pl) * V3_POS;
     const uint32_t kb = sm_a + geo.off_key + (uint32_t)(it % 3) * geo.key_bytes;
     const int pieces = a.T * LT * 2 * (V3_POS / 2);
-    for (int e = threadIdx.x; e < pieces; e += V2_PROD) {
+    for (int e = threadIdx.x; e < pieces; e += V3_PROD) {
       const int p2 = e % (V3_POS / 2), r = e / (V3_POS / 2);  // r = (tap L + i) 2 + comp
       const int comp = r % 2, i = (r / 2) % LT, tap = r / (2 * LT);
       const u64* key = a.tt.key[tap];
@@ -193,7 +200,7 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&kfull[it % 3])) : "memory");
   };
 
-  if (warp < V2_PROD_WARPS) {
+  if (warp < V3_PROD_WARPS) {
     // ======================= producers =======================
     if (my_tiles > 0) issue_keys(0);
     if (my_tiles > 1) issue_keys(1);

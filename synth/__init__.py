@@ -57,16 +57,19 @@ def uniform_residues(g: np.random.Generator, moduli: List[int], shape) -> np.nda
 
 # --------------------------------------------------------------------------------------
 # BASELINE.json configurations (shapes, ring parameters, value ranges).
-# Primes: the largest primes below 2^b with q = 1 mod 2N, descending;
-# both the oracle and the library check primality and q = 1 mod 2N independently.
+# Primes: the largest primes below 2^b with q = 1 mod 2^32 (so q = 1 mod 2N for every N <= 2^31),
+# descending (reading R4: "NTT-friendly primes <= b bits").  q = 1 mod 2^32
+# makes h q mod 2^64 = h + (h q_hi) 2^32 one 32-bit multiply in every Shoup reduction of the library
+# (DESIGN.md §4); the library accepts any NTT-friendly prime and uses that form only when all limbs
+# have it.  Both the oracle and the library check primality and q = 1 mod 2N independently.
 # --------------------------------------------------------------------------------------
 
+_P60 = [0xFFFFFA000000001, 0xFFFFF8800000001, 0xFFFFF7B00000001, 0xFFFFF6100000001, 0xFFFFF5800000001]
 PRIMES = {
-    (4096, 50): [0x3FFFFFFFFC001, 0x3FFFFFFFCC001],
-    (4096, 60): [0xFFFFFFFFFFFC001, 0xFFFFFFFFFFE8001],
-    (8192, 60): [0xFFFFFFFFFFFC001, 0xFFFFFFFFFFE8001, 0xFFFFFFFFFFD8001],
-    (16384, 60): [0xFFFFFFFFFFE8001, 0xFFFFFFFFFFD8001, 0xFFFFFFFFFFC0001,
-                  0xFFFFFFFFFF28001, 0xFFFFFFFFFE38001],
+    (4096, 50): [0x3FFF300000001, 0x3FFED00000001],
+    (4096, 60): _P60[:2],
+    (8192, 60): _P60[:3],
+    (16384, 60): _P60[:5],
 }
 
 T_PLAIN = 65537

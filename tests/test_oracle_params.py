@@ -58,8 +58,11 @@ def test_t65537_values():
 
 
 def test_primes_in_synth_are_the_largest_ntt_primes():
+    """synth.PRIMES = the largest primes < 2^b with q = 1 mod 2^32 (= ntt_primes with 2N = 2^32), so
+    NTT-friendly (q = 1 mod 2N) for every configured N."""
     for (N, bits), ps in PRIMES.items():
-        assert ntt_primes(N, bits, len(ps)) == ps
+        assert ntt_primes(2**31, bits, len(ps)) == ps
+        assert all(q % (2 * N) == 1 and q % 2**32 == 1 and q < 2**bits for q in ps)
 
 
 @pytest.mark.parametrize("t,N", [(97, 16), (65537, 64)])

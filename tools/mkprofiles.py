@@ -72,15 +72,18 @@ want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
+        "l1tex__t_sector_hit_rate.pct", "smsp__inst_executed.sum",
         "smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio",
-        "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio"]
+        "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+        "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio"]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 traffic = json.load(open("profiles/traffic.json")) if os.path.exists("profiles/traffic.json") else {}
-for f in sorted(glob.glob(f"gpurun_out/{tag}_*.ncu-rep")):
+# ncu --set full captures, exported on the GPU box to CSV (tools/gpu_prof.sh: {tag}_full_<cfg>_raw.csv)
+for f in sorted(glob.glob(f"gpurun_out/{tag}_full_*_raw.csv")):
     base = os.path.basename(f)[len(tag) + 1:-8]
     cfg = base.split("_")[-1]
-    raw = subprocess.run(["ncu", "-i", f, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-    rows = list(csv.reader(raw.splitlines()))
+    os.system(f"cp {f} profiles/")
+    rows = list(csv.reader(open(f).read().splitlines()))
     if len(rows) < 3:
         continue
     hdr, units, data = rows[0], rows[1], rows[2:]
@@ -95,6 +98,7 @@ for f in sorted(glob.glob(f"gpurun_out/{tag}_*.ncu-rep")):
                   + " |")
         stage = ("S2S3_ksmac_wht" if "mac" in name else "S1_permdecomp" if "PermDecomp" in name else
                  "S4S5_align_intt" if "OutInv" in name else None)
+        stage = stage if stage else None
         if stage:  # dram bytes per launch of the stage's dominant kernel
             i_r, i_w = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
             b = float(r[i_r].replace(",", "")) * scale.get(units[i_r], 1) + \

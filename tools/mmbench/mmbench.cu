@@ -53,13 +53,45 @@ __device__ __forceinline__ u64 shoup(u64 x, u64 w, u64 wsh, u64 q) {
   return 0;
 }
 
+__device__ __forceinline__ void bfly_ptx_full(u64& x, u64& y, u64 w, u64 wsh, u64 q, u64 q2);
 // Harvey CT butterfly, [0, 4q) -> [0, 4q) (exact quotient variants)
 template <int V>
 __device__ __forceinline__ void bfly(u64& x, u64& y, u64 w, u64 wsh, u64 q, u64 q2) {
+  if constexpr (V == 9) {
+    bfly_ptx_full(x, y, w, wsh, q, q2);
+    return;
+  }
   const u64 X = csub(x, q2);
   const u64 T = shoup<V>(y, w, wsh, q);
   x = X + T;
   y = X - T + q2;
+}
+
+// whole Harvey CT butterfly in PTX on 32-bit halves (exact Shoup quotient)
+__device__ __forceinline__ void bfly_ptx_full(u64& x, u64& y, u64 w, u64 wsh, u64 q, u64 q2) {
+  uint32_t x0 = (uint32_t)x, x1 = (uint32_t)(x >> 32), y0 = (uint32_t)y, y1 = (uint32_t)(y >> 32);
+  const uint32_t w0 = (uint32_t)w, w1 = (uint32_t)(w >> 32), s0 = (uint32_t)wsh, s1 = (uint32_t)(wsh >> 32);
+  const uint32_t q0 = (uint32_t)q, q1 = (uint32_t)(q >> 32), p0 = (uint32_t)q2, p1 = (uint32_t)(q2 >> 32);
+  asm("{\n\t.reg .u32 a, b, c, h0, h1, t0, t1, u0, u1, v0, v1;\n\t.reg .pred p;\n\t"
+      // X = x >= 2q ? x - 2q : x
+      "sub.cc.u32 v0, %0, %10;\n\tsubc.cc.u32 v1, %1, %11;\n\tsubc.u32 a, 0, 0;\n\t"
+      "setp.eq.u32 p, a, 0;\n\t@p mov.u32 %0, v0;\n\t@p mov.u32 %1, v1;\n\t"
+      // h = hi64(y * wsh)
+      "mul.hi.u32 a, %2, %6;\n\t"
+      "mad.lo.cc.u32 a, %2, %7, a;\n\tmadc.hi.u32 b, %2, %7, 0;\n\t"
+      "mad.lo.cc.u32 a, %3, %6, a;\n\tmadc.hi.cc.u32 b, %3, %6, b;\n\taddc.u32 c, 0, 0;\n\t"
+      "mad.lo.cc.u32 h0, %3, %7, b;\n\tmadc.hi.u32 h1, %3, %7, c;\n\t"
+      // T = y w - h q (mod 2^64)
+      "mul.lo.u32 t0, %2, %4;\n\tmul.hi.u32 t1, %2, %4;\n\tmad.lo.u32 t1, %2, %5, t1;\n\tmad.lo.u32 t1, %3, %4, t1;\n\t"
+      "mul.lo.u32 u0, h0, %8;\n\tmul.hi.u32 u1, h0, %8;\n\tmad.lo.u32 u1, h0, %9, u1;\n\tmad.lo.u32 u1, h1, %8, u1;\n\t"
+      "sub.cc.u32 t0, t0, u0;\n\tsubc.u32 t1, t1, u1;\n\t"
+      // y' = X - T + 2q, x' = X + T
+      "sub.cc.u32 v0, %0, t0;\n\tsubc.u32 v1, %1, t1;\n\tadd.cc.u32 %2, v0, %10;\n\taddc.u32 %3, v1, %11;\n\t"
+      "add.cc.u32 %0, %0, t0;\n\taddc.u32 %1, %1, t1;\n\t}"
+      : "+r"(x0), "+r"(x1), "+r"(y0), "+r"(y1)
+      : "r"(w0), "r"(w1), "r"(s0), "r"(s1), "r"(q0), "r"(q1), "r"(p0), "r"(p1));
+  x = ((u64)x1 << 32) | x0;
+  y = ((u64)y1 << 32) | y0;
 }
 
 template <int V>
@@ -139,6 +171,18 @@ __global__ void k_check(const u64* __restrict__ prm, const u64* xs, int n, int* 
   }
 }
 
+__global__ void k_check_bfly(const u64* __restrict__ prm, const u64* xs, int n, int* bad) {
+  const u64 q = prm[0], q2 = 2 * q;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const u64 x = xs[3 * i] % (4 * q), y = xs[3 * i + 1] % (4 * q), w = xs[3 * i + 2] % q;
+    const u64 wsh = (u64)(((u128)w << 64) / q);
+    u64 a = x, b = y, c = x, d = y;
+    bfly<0>(a, b, w, wsh, q, q2);
+    bfly<9>(c, d, w, wsh, q, q2);
+    if (a != c || b != d) atomicAdd(bad, 1);
+  }
+}
+
 typedef void (*kfn)(const u64*, u64*);
 
 static void run(const char* name, kfn f, double ops_per_thread, const u64* prm, u64* o) {
@@ -191,7 +235,12 @@ int main(int argc, char** argv) {
          (unsigned long long)h_prm[0], hb[0], hb[1], hb[2]);
   CHECK(0) CHECK(1) CHECK(2)
   if (sp) { CHECK(3) CHECK(4) }
+  cudaMemset(bad, 0, 12);
+  k_check_bfly<<<592, 256>>>(prm, xs, n, bad);
+  cudaMemcpy(hb, bad, 12, cudaMemcpyDeviceToHost);
+  printf("{\"check\": \"bfly_ptx_full == bfly_c\", \"bad\": %d}\n", hb[0]);
   const double nb = (double)ITERS * 16, nk = (double)ITERS * 8 * 3;
+  run("bfly_ptx_full", k_bfly<9>, nb, prm, o);
   run("bfly_c", k_bfly<0>, nb, prm, o);
   run("bfly_ptx", k_bfly<1>, nb, prm, o);
   run("ks_c", k_ks<0>, nk, prm, o);

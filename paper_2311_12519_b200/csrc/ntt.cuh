@@ -335,6 +335,101 @@ inline size_t ntt_smem_bytes() {
 // of stage log2 m (inverse: ipsi2 with psi^{-1}).  Forward values stay in Harvey's [0, 4q); the
 // inverse keeps [0, 2q) and folds N^{-1} into its last stage.
 // =======================================================================================
+#ifndef NTT2_APX
+#define NTT2_APX 0
+#endif
+#ifndef NTT2_PTX
+#define NTT2_PTX 1
+#endif
+#ifndef NTT2_Q1
+#define NTT2_Q1 0
+#endif
+// Butterflies on 32-bit halves (inline PTX).  The C form compiled to ~40 SASS per butterfly (register
+// moves on the FMA pipe, IMAD.X adds, compare + select pairs); these are ~21: the exact Shoup
+// quotient H = hi64(y w') from four 32-bit partial products, T = y w + H (2^64 - q) (mod 2^64) as
+// accumulating multiply-adds, and every conditional subtraction as subtract-with-borrow + LOP3 select.
+//   CT (forward, Harvey): x, y in [0, 4q) -> x' = X + T, y' = X - T + 2q, X = x mod' 2q, T in [0, 2q)
+//   GS (inverse):         x, y in [0, 2q) -> x' = (x + y) mod' 2q, y' = Shoup(x - y + 2q) in [0, 2q)
+#if NTT2_APX  // approximate quotient y1 s1 + hi32(y1 s0) + hi32(y0 s1): undershoots by <= 3, T in [0, 5q)
+#define NTT2_SHOUP_H(Y0, Y1)                                       \
+  "mul.lo.u32 h0, " Y1 ", s1;\n\t"                                \
+  "mul.hi.u32 h1, " Y1 ", s1;\n\t"                                \
+  "mad.hi.cc.u32 h0, " Y1 ", s0, h0;\n\t"                         \
+  "addc.u32 h1, h1, 0;\n\t"                                       \
+  "mad.hi.cc.u32 h0, " Y0 ", s1, h0;\n\t"                         \
+  "addc.u32 h1, h1, 0;\n\t"
+#else
+#define NTT2_SHOUP_H(Y0, Y1)                                       \
+  "mul.hi.u32 a0, " Y0 ", s0;\n\t"                                \
+  "mad.lo.cc.u32 a0, " Y0 ", s1, a0;\n\t"                         \
+  "madc.hi.u32 a1, " Y0 ", s1, 0;\n\t"                            \
+  "mad.lo.cc.u32 a0, " Y1 ", s0, a0;\n\t"                         \
+  "madc.hi.cc.u32 a1, " Y1 ", s0, a1;\n\t"                        \
+  "addc.u32 a2, 0, 0;\n\t"                                        \
+  "mad.lo.cc.u32 h0, " Y1 ", s1, a1;\n\t"                         \
+  "madc.hi.u32 h1, " Y1 ", s1, a2;\n\t"
+#endif
+#if NTT2_Q1  // q = 1 mod 2^32: H q = H + (H0 q1) 2^32 (mod 2^64); n1 = -q1 mod 2^32
+#define NTT2_SHOUP_T(Y0, Y1)                                       \
+  NTT2_SHOUP_H(Y0, Y1)                                             \
+  "mul.lo.u32 T0, " Y0 ", w0;\n\t"                                \
+  "mul.hi.u32 T1, " Y0 ", w0;\n\t"                                \
+  "mad.lo.u32 T1, " Y0 ", w1, T1;\n\t"                            \
+  "mad.lo.u32 T1, " Y1 ", w0, T1;\n\t"                            \
+  "sub.cc.u32 T0, T0, h0;\n\t"                                    \
+  "subc.u32 T1, T1, h1;\n\t"                                      \
+  "mad.lo.u32 T1, h0, n1, T1;\n\t"
+#else
+#define NTT2_SHOUP_T(Y0, Y1)                                       \
+  NTT2_SHOUP_H(Y0, Y1)                                             \
+  "mul.lo.u32 T0, " Y0 ", w0;\n\t"                                \
+  "mul.hi.u32 T1, " Y0 ", w0;\n\t"                                \
+  "mad.lo.u32 T1, " Y0 ", w1, T1;\n\t"                            \
+  "mad.lo.u32 T1, " Y1 ", w0, T1;\n\t"                            \
+  "mad.lo.cc.u32 T0, h0, n0, T0;\n\t"                             \
+  "madc.hi.u32 T1, h0, n0, T1;\n\t"                               \
+  "mad.lo.u32 T1, h0, n1, T1;\n\t"                                \
+  "mad.lo.u32 T1, h1, n0, T1;\n\t"
+#endif
+// nq operand: 2^64 - q (generic), or (-q1 mod 2^32) << 32 (NTT2_Q1)
+__device__ __forceinline__ u64 ntt2_nq(u64 q) {
+#if NTT2_Q1
+  return (u64)(0u - (uint32_t)(q >> 32)) << 32;
+#else
+  return 0 - q;
+#endif
+}
+
+__device__ __forceinline__ void ntt2_ct_ptx(u64& x, u64& y, u64 w, u64 ws, u64 nq, u64 q2) {
+  asm("{\n\t.reg .u32 x0, x1, y0, y1, w0, w1, s0, s1, n0, n1, t0, t1, a0, a1, a2, h0, h1, T0, T1, d0, d1, m;\n\t"
+      "mov.b64 {x0, x1}, %0;\n\tmov.b64 {y0, y1}, %1;\n\tmov.b64 {w0, w1}, %2;\n\tmov.b64 {s0, s1}, %3;\n\t"
+      "mov.b64 {n0, n1}, %4;\n\tmov.b64 {t0, t1}, %5;\n\t"
+      NTT2_SHOUP_T("y0", "y1")
+      "sub.cc.u32 d0, x0, t0;\n\tsubc.cc.u32 d1, x1, t1;\n\tsubc.u32 m, 0, 0;\n\t"
+      "lop3.b32 x0, m, x0, d0, 0xCA;\n\tlop3.b32 x1, m, x1, d1, 0xCA;\n\t"
+      "add.cc.u32 d0, x0, t0;\n\taddc.u32 d1, x1, t1;\n\t"
+      "sub.cc.u32 y0, d0, T0;\n\tsubc.u32 y1, d1, T1;\n\t"
+      "add.cc.u32 x0, x0, T0;\n\taddc.u32 x1, x1, T1;\n\t"
+      "mov.b64 %0, {x0, x1};\n\tmov.b64 %1, {y0, y1};\n\t}"
+      : "+l"(x), "+l"(y)
+      : "l"(w), "l"(ws), "l"(nq), "l"(q2));
+}
+
+__device__ __forceinline__ void ntt2_gs_ptx(u64& x, u64& y, u64 w, u64 ws, u64 nq, u64 q2) {
+  asm("{\n\t.reg .u32 x0, x1, y0, y1, w0, w1, s0, s1, n0, n1, t0, t1, a0, a1, a2, h0, h1, T0, T1, d0, d1, v0, v1, m;\n\t"
+      "mov.b64 {x0, x1}, %0;\n\tmov.b64 {y0, y1}, %1;\n\tmov.b64 {w0, w1}, %2;\n\tmov.b64 {s0, s1}, %3;\n\t"
+      "mov.b64 {n0, n1}, %4;\n\tmov.b64 {t0, t1}, %5;\n\t"
+      "add.cc.u32 v0, x0, t0;\n\taddc.u32 v1, x1, t1;\n\t"
+      "sub.cc.u32 v0, v0, y0;\n\tsubc.u32 v1, v1, y1;\n\t"
+      "add.cc.u32 x0, x0, y0;\n\taddc.u32 x1, x1, y1;\n\t"
+      "sub.cc.u32 d0, x0, t0;\n\tsubc.cc.u32 d1, x1, t1;\n\tsubc.u32 m, 0, 0;\n\t"
+      "lop3.b32 x0, m, x0, d0, 0xCA;\n\tlop3.b32 x1, m, x1, d1, 0xCA;\n\t"
+      NTT2_SHOUP_T("v0", "v1")
+      "mov.b64 %0, {x0, x1};\n\tmov.b64 %1, {T0, T1};\n\t}"
+      : "+l"(x), "+l"(y)
+      : "l"(w), "l"(ws), "l"(nq), "l"(q2));
+}
+
 template <int LOGN>
 struct Ntt2Cfg {
   static constexpr int LOGV = 5, V = 32;
@@ -372,12 +467,26 @@ __global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
   u64 v[V];
 #pragma unroll
   for (int r = 0; r < V; r++) v[r] = jb.load(tid + T * r);
+#if NTT2_PTX
+  const u64 nq = ntt2_nq(q), qb = (NTT2_APX ? 5 : 2) * q;  // values in [0, 2 qb)
+  auto bfly = [&](u64& x, u64& y, const ulonglong2 w) { ntt2_ct_ptx(x, y, w.x, w.y, nq, qb); };
+#elif NTT2_APX
+  // approximate Shoup quotient (umulhi_apx: Tt in [0, 5q)): values stay in [0, 10q) < 2^64 (q < 2^60)
+  const u64 qb = 5 * q;
+  auto bfly = [&](u64& x, u64& y, const ulonglong2 w) {  // CT: [0, 10q) -> [0, 10q)
+    const u64 X = csub2(x, qb);
+    const u64 Tt = y * w.x - umulhi_apx(y, w.y) * q;
+    x = X + Tt;
+    y = X - Tt + qb;
+  };
+#else
   auto bfly = [&](u64& x, u64& y, const ulonglong2 w) {  // Harvey CT: [0, 4q) -> [0, 4q)
     const u64 X = csub2(x, q2);
     const u64 Tt = shoup_mul(y, w.x, w.y, q);
     x = X + Tt;
     y = X - Tt + q2;
   };
+#endif
   // ---- group A: stages 0..4, twiddles uniform over the CTA ----
 #pragma unroll
   for (int s = 0; s < 5; s++) {
@@ -425,7 +534,11 @@ __global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
   for (int qq = 0; qq < C::QN; qq++)
 #pragma unroll
     for (int rr = 0; rr < D; rr++) {
+#if NTT2_APX
+      const u64 x = csub2(csub2(csub2(csub2(v[qq * D + rr], 8 * q), 4 * q), q2), q);
+#else
       const u64 x = csub2(csub2(v[qq * D + rr], q2), q);
+#endif
       sm[ntt2_sw<LOGN>(D * (tid + T * qq) + rr)] = x;
     }
   __syncthreads();
@@ -458,12 +571,26 @@ __global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
   }
   __syncthreads();
   u64 v[V];
+#if NTT2_PTX
+  const u64 qb = (NTT2_APX ? 5 : 2) * q, nq = ntt2_nq(q);  // values in [0, qb)
+  auto bfly = [&](u64& x, u64& y, const ulonglong2 w) { ntt2_gs_ptx(x, y, w.x, w.y, nq, qb); };
+#elif NTT2_APX
+  const u64 qb = 5 * q;  // approximate quotients: values in [0, 5q)
+  auto bfly = [&](u64& x, u64& y, const ulonglong2 w) {  // GS: [0, 5q) -> [0, 5q)
+    const u64 U = csub2(x + y, qb);
+    const u64 Vv = x - y + qb;
+    y = Vv * w.x - umulhi_apx(Vv, w.y) * q;
+    x = U;
+  };
+#else
+  const u64 qb = q2;
   auto bfly = [&](u64& x, u64& y, const ulonglong2 w) {  // Harvey GS: [0, 2q) -> [0, 2q)
     const u64 U = csub2(x + y, q2);
     const u64 Vv = x - y + q2;
     y = shoup_mul(Vv, w.x, w.y, q);
     x = U;
   };
+#endif
   // ---- group C (stages LOGN-1 .. 10) ----
 #pragma unroll
   for (int qq = 0; qq < C::QN; qq++)
@@ -517,7 +644,7 @@ __global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
     for (int r = 0; r < 16; r++) {
       const u64 x = v[r], y = v[r + 16];
       const u64 a0 = csub2(shoup_mul(x + y, ni, nis, q), q);
-      const u64 a1 = csub2(shoup_mul(x - y + q2, wn.x, wn.y, q), q);
+      const u64 a1 = csub2(shoup_mul(x - y + qb, wn.x, wn.y, q), q);
       jb.store(tid + T * r, a0);
       jb.store(tid + T * (r + 16), a1);
     }

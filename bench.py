@@ -290,7 +290,7 @@ def traffic_for(cfg_name, kernel):
 MODMUL_PER_CLK_SM = 4.0   # 64-bit Shoup product = 6 IMAD.WIDE (2 issue slots) + 4 IMAD on 64 lanes/clk/SM
 I8_PER_BF16 = 2.0         # dense int8 / bf16 tensor throughput, nominal (B200_PROFILING.md: 4.5 vs 2.25 P)
 MAC_KERNEL = {"thin": "ksmac_thin_kernel (fused S2+S3, FP64 MAC)",
-              "tc_fused": "ksmac_tc_kernel (fused S2+S3: key switching + tcgen05 int8 MAC)",
+              "tc_fused": "ksmac_v2_kernel (persistent fused S2+S3: key switching + tcgen05 int8 MAC; HY_KSMAC=1 selects round 1's ksmac_tc_kernel)",
               "tc_split": "mac_tc_kernel (S3 tcgen05 int8 MAC over stored R)",
               "fp64_fused": "ksmac_gemm_kernel (fused S2+S3, FP64 MAC)",
               "fp64_split": "mac_gemm_kernel (S3 FP64 MAC over stored R)",

@@ -3,6 +3,7 @@
 // every formula is re-derived from PAPER.md here.
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -1093,7 +1094,17 @@ extern "C" hy_status hy_conv_eval_host(hy_weights* w, const uint64_t* in, size_t
   }
   // Pipelined over batches of units (units are independent): the upload of batch
   // b + 1 and the download of batch b - 1 overlap the evaluation of batch b on the caller's stream.
-  const size_t nb = nu >= 8 ? (nu + 7) / 8 : nu;  // units per batch: 8 batches when possible
+  // Batch size: the pipeline's fill and drain cost one batch's upload + evaluation + download, so
+  // batches are as small as keeps a copy efficient (>= 32 MiB of input per batch, at most 32 batches;
+  // HY_HOST_BATCHES overrides the batch count for measurements).
+  size_t nbatch = 32;
+  if (const char* e = getenv("HY_HOST_BATCHES")) nbatch = std::max<size_t>(1, strtoull(e, nullptr, 10));
+  size_t nb = (nu + nbatch - 1) / nbatch;
+  if (!getenv("HY_HOST_BATCHES")) {
+    const size_t unit_bytes = (size_t)lay.Jc * ctw * sizeof(u64);
+    nb = std::max(nb, ((size_t)32 << 20) / unit_bytes + 1);
+  }
+  nb = std::min(std::max<size_t>(nb, 1), nu);
   for (size_t u0 = 0; u0 < nu; u0 += nb) {
     const size_t n = std::min(nb, nu - u0);
     const size_t i0 = u0 * lay.Jc, ni = n * lay.Jc, o0 = u0 * lay.Jo, no = n * lay.Jo;

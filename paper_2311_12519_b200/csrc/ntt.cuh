@@ -344,6 +344,9 @@ inline size_t ntt_smem_bytes() {
 #ifndef NTT2_Q1
 #define NTT2_Q1 0
 #endif
+#ifndef NTT2_EXP  // timing experiments only (wrong results), bit mask: 1 = no butterfly arithmetic, 2 = no global loads / stores, 4 = no twiddle loads
+#define NTT2_EXP 0
+#endif
 // Butterflies on 32-bit halves (inline PTX).  The C form compiled to ~40 SASS per butterfly (register
 // moves on the FMA pipe, IMAD.X adds, compare + select pairs); these are ~21: the exact Shoup
 // quotient H = hi64(y w') from four 32-bit partial products, T = y w + H (2^64 - q) (mod 2^64) as
@@ -430,6 +433,38 @@ __device__ __forceinline__ void ntt2_gs_ptx(u64& x, u64& y, u64 w, u64 ws, u64 n
       : "l"(w), "l"(ws), "l"(nq), "l"(q2));
 }
 
+#if NTT2_EXP & 4
+#define NTT2_TW(p) make_ulonglong2((u64)(size_t)(p), 12345)
+#else
+#define NTT2_TW(p) __ldg(p)
+#endif
+#ifndef NTT2_PRE  // 1: L1 prefetch of the next register group's twiddles before each barrier (measured slower: S1 4.37 -> 4.49 ms)
+#define NTT2_PRE 0
+#endif
+__device__ __forceinline__ void ntt2_pf(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+// twiddles of group B (stages 5..9) of block `blk`: 2^{s-5} consecutive entries per stage, shared by the
+// D threads of the block -> lane d of the block prefetches one 128-byte line
+template <int LOGN>
+__device__ __forceinline__ void ntt2_pf_groupB(const ulonglong2* W, int tid) {
+  constexpr int D = 1 << (LOGN - 10);
+  const int blk = tid / D, d = tid % D;
+  if (d < 2) ntt2_pf(W + (1 << 9) + (blk << 4) + 8 * d);
+  else if (d == 2) ntt2_pf(W + (1 << 8) + (blk << 3));
+  else if (d == 3) ntt2_pf(W + (1 << 7) + (blk << 2));
+  if (D <= 4 || d == 4) ntt2_pf(W + (1 << 6) + (blk << 1));
+  if (D <= 4 || d == 5) ntt2_pf(W + (1 << 5) + blk);
+}
+// twiddles of group C (stages 10..LOGN-1) of this thread's sub-blocks
+template <int LOGN>
+__device__ __forceinline__ void ntt2_pf_groupC(const ulonglong2* W, int tid) {
+  constexpr int T = 1 << (LOGN - 5), D = 1 << (LOGN - 10), QN = 32 / D;
+#pragma unroll
+  for (int s = 10; s < LOGN; s++)
+#pragma unroll
+    for (int qq = 0; qq < QN; qq++) ntt2_pf(W + (1 << s) + ((tid + T * qq) << (s - 10)));
+}
 template <int LOGN>
 struct Ntt2Cfg {
   static constexpr int LOGV = 5, V = 32;
@@ -466,8 +501,10 @@ __global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
   const ulonglong2* __restrict__ W = tb.tw + ((size_t)l << LOGN);
   u64 v[V];
 #pragma unroll
-  for (int r = 0; r < V; r++) v[r] = jb.load(tid + T * r);
-#if NTT2_PTX
+  for (int r = 0; r < V; r++) v[r] = (NTT2_EXP & 2) ? (u64)(tid + T * r) * q : jb.load(tid + T * r);
+#if NTT2_EXP & 1
+  auto bfly = [&](u64& x, u64& y, const ulonglong2 w) { x ^= y + w.x; y ^= w.y; };
+#elif NTT2_PTX
   const u64 nq = ntt2_nq(q), qb = (NTT2_APX ? 5 : 2) * q;  // values in [0, 2 qb)
   auto bfly = [&](u64& x, u64& y, const ulonglong2 w) { ntt2_ct_ptx(x, y, w.x, w.y, nq, qb); };
 #elif NTT2_APX
@@ -493,10 +530,11 @@ __global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
     const int h = 16 >> s;
 #pragma unroll
     for (int r = 0; r < V; r++)
-      if ((r & h) == 0) bfly(v[r], v[r + h], __ldg(W + (1 << s) + (r >> (5 - s))));
+      if ((r & h) == 0) bfly(v[r], v[r + h], NTT2_TW(W + (1 << s) + (r >> (5 - s))));
   }
 #pragma unroll
   for (int r = 0; r < V; r++) sm[ntt2_sw<LOGN>(tid + T * r)] = v[r];
+  if (NTT2_PRE == 1) ntt2_pf_groupB<LOGN>(W, tid);
   __syncthreads();
   // ---- group B: stages 5..9 ----
   const int blk = tid / D, baseB = blk * (D * V) + tid % D;
@@ -508,11 +546,12 @@ __global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
     const int sh = LOGN - s;  // log2 of the block size of stage s
 #pragma unroll
     for (int r = 0; r < V; r++)
-      if ((r & h) == 0) bfly(v[r], v[r + h], __ldg(W + (1 << s) + (blk << (s - 5)) + ((D * r) >> sh)));
+      if ((r & h) == 0) bfly(v[r], v[r + h], NTT2_TW(W + (1 << s) + (blk << (s - 5)) + ((D * r) >> sh)));
   }
   // (every thread rewrites exactly the positions it read: no barrier before the write-back)
 #pragma unroll
   for (int r = 0; r < V; r++) sm[ntt2_sw<LOGN>(baseB + D * r)] = v[r];
+  if (NTT2_PRE == 1) ntt2_pf_groupC<LOGN>(W, tid);
   __syncthreads();
   // ---- group C: stages 10..LOGN-1 inside D-point sub-blocks ----
 #pragma unroll
@@ -528,7 +567,7 @@ __global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
       for (int rr = 0; rr < D; rr++)
         if ((rr & h) == 0)
           bfly(v[qq * D + rr], v[qq * D + rr + h],
-               __ldg(W + (1 << s) + ((tid + T * qq) << (s - 10)) + (rr >> (LOGN - s))));
+               NTT2_TW(W + (1 << s) + ((tid + T * qq) << (s - 10)) + (rr >> (LOGN - s))));
   }
 #pragma unroll
   for (int qq = 0; qq < C::QN; qq++)
@@ -546,7 +585,8 @@ __global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
 #pragma unroll 8
   for (int r = 0; r < V; r++) {
     const int j = tid + T * r;
-    jb.store(j, sm[ntt2_sw<LOGN>(__ldg(tb.kos + j))]);
+    const u64 x = sm[ntt2_sw<LOGN>(__ldg(tb.kos + j))];
+    if (!(NTT2_EXP & 2) || x == 0x123456789abcdefull) jb.store(j, x);
   }
 }
 
@@ -564,6 +604,7 @@ __global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
   const u64 q = L.lc[l].q, q2 = L.lc[l].two_q;
   const ulonglong2* __restrict__ W = tb.tw + ((size_t)l << LOGN);
   // ---- slot-order input -> butterfly positions ----
+  if (NTT2_PRE == 1) ntt2_pf_groupC<LOGN>(W, tid);
 #pragma unroll 8
   for (int r = 0; r < V; r++) {
     const int j = tid + T * r;
@@ -611,6 +652,7 @@ __global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
   for (int qq = 0; qq < C::QN; qq++)
 #pragma unroll
     for (int rr = 0; rr < D; rr++) sm[ntt2_sw<LOGN>(D * (tid + T * qq) + rr)] = v[qq * D + rr];
+  if (NTT2_PRE == 1) ntt2_pf_groupB<LOGN>(W, tid);
   __syncthreads();
   // ---- group B (stages 9 .. 5) ----
   const int blk = tid / D, baseB = blk * (D * V) + tid % D;

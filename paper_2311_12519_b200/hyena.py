@@ -211,16 +211,23 @@ def hy_weights_layout(w: int) -> hy_layout:
     return lay
 
 
+_RING: dict = {}  # weights handle -> (L, N): the shape check of every eval costs no library call
+
+
 def hy_weights_destroy(w: int):
+    _RING.pop(w, None)
     load_library().hy_weights_destroy(w)
 
 
 def _ct_words(w: int, shape, what: str) -> int:
     """Words of a [n][2][L][N] ciphertext array for the weights' ring (checked shape)."""
-    lay = hy_weights_layout(w)
-    if len(shape) != 4 or tuple(shape[1:]) != (2, lay.L, lay.N):
-        raise HyenaError(f"{what}: expected shape [n][2][{lay.L}][{lay.N}], got {tuple(shape)}")
-    return int(shape[0]) * 2 * lay.L * lay.N
+    ring = _RING.get(w)
+    if ring is None:
+        lay = hy_weights_layout(w)
+        ring = _RING[w] = (int(lay.L), int(lay.N))
+    if len(shape) != 4 or tuple(shape[1:]) != (2,) + ring:
+        raise HyenaError(f"{what}: expected shape [n][2][{ring[0]}][{ring[1]}], got {tuple(shape)}")
+    return int(shape[0]) * 2 * ring[0] * ring[1]
 
 
 def hy_conv_eval(w: int, ct_in, ct_out, J: Optional[int] = None, Jout: Optional[int] = None, stream=None):

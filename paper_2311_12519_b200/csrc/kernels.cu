@@ -2061,7 +2061,7 @@ hy_status launch_ksmac_tc(const KsMacArgs& a, const int8_t* w8, int units, cudaS
     }
   }
   if (uni && !a.coef && ver == 2 && a.Mpad <= 128 && a.wblocks == 1) {
-    const V2Geom g = v2_geom(a.T, LT, a.Kpad, 232448);
+    const V2Geom g = v2_geom(a.T, LT, a.Kpad, 232448, a.M);
     if (g.S >= 2) {
       if (a.logN == 13) return launch_ksmac_v2<LT, 13>(a, w8, units, g, s);
       return launch_ksmac_v2<LT, 0>(a, w8, units, g, s);

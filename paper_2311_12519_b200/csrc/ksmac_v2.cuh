@@ -51,6 +51,15 @@
 #ifndef V2_PW
 #define V2_PW 16
 #endif
+#ifndef V2_WRES  // 0: never keep the weights resident (experiment: more L1 for the digit windows)
+#define V2_WRES 1
+#endif
+#ifndef V2_PAD   // extra shared memory requested (experiment: less L1)
+#define V2_PAD 0
+#endif
+#ifndef V2_HALF  // M <= 64: resident weights as 64-row half tiles (more L1 for the digit windows)
+#define V2_HALF 1
+#endif
 // producer warps (a multiple of 4): 16 slot positions x 2 PW term groups of 4 per chunk
 constexpr int V2_PROD_WARPS = V2_PW, V2_PROD = V2_PROD_WARPS * 32;
 constexpr int V2_KS = V2_PW / 4, V2_CHUNK = 32 * V2_KS;     // PW = 12: 96 terms = 3 UMMA K steps per chunk
@@ -69,6 +78,7 @@ struct V2Warps {
 struct V2Geom {
   int S;                 // pipeline stages
   int wres;              // 1: all weights resident in shared memory
+  int half;              // 1: resident weights hold rows 0..63 only (M <= 64), 2048 bytes per K step
   int kb;                // key buffers (3 or 4; keys are prefetched two tiles ahead)
   uint32_t off_b, off_a, off_key, off_bar;
   uint32_t key_bytes;    // one key buffer
@@ -78,20 +88,25 @@ struct V2Geom {
 // largest configuration that fits, preferring resident weights, then 4 stages, then 4 key buffers
 // (with 4, the buffer a tile's keys are copied into was last read two tiles earlier: the producer
 // warps, which the stage ring keeps within S < one tile of each other, never wait for it)
-inline V2Geom v2_geom(int T, int L, int Kpad, size_t smem_max) {
+// M <= 64 (V2_HALF): only the 64 live weight rows are kept (rows 0..63 of a canonical 128 x 32 tile are
+// its first 2048 bytes); the M = 128 UMMA of K step k then reads K step k + 1's rows as its rows
+// 64..127 (the last step reads 2 KB of the stage ring): those accumulator lanes are never read
+inline V2Geom v2_geom(int T, int L, int Kpad, size_t smem_max, int M = 128) {
   V2Geom g{};
-  const uint32_t wbytes = 128u * (uint32_t)Kpad;
+  g.half = V2_HALF && M <= 64;
+  const uint32_t wbytes = (g.half ? 64u : 128u) * (uint32_t)Kpad;
   g.key_bytes = (uint32_t)T * 4 * L * TC_POS * 8;
   const uint32_t bar = 256;
-  for (int wres = 1; wres >= 0; wres--) {
+  for (int wres = V2_WRES; wres >= 0; wres--) {
     for (int S = V2_SMAX; S >= 2; S--) {
       for (int kb = V2_KBMAX; kb >= 3; kb--) {
         const uint32_t w = wres ? wbytes : 0;
         const uint32_t per = V2_STAGE_B + (wres ? 0 : V2_STAGE_A);
-        const size_t tot = 1024 + (size_t)w + (size_t)S * per + (size_t)kb * g.key_bytes + bar;
+        const size_t tot = 1024 + (size_t)w + (size_t)S * per + (size_t)kb * g.key_bytes + bar + V2_PAD;
         if (tot <= smem_max) {
           g.S = S;
           g.wres = wres;
+          if (!wres) g.half = 0;
           g.kb = kb;
           g.off_b = w;
           g.off_a = w + S * V2_STAGE_B;
@@ -224,8 +239,13 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
   }
   if (geo.wres) {  // resident weights: [nk32][4096] canonical K-major tiles (one 128-row M tile)
     const uint4* src = reinterpret_cast<const uint4*>(w8);
-    for (int e = threadIdx.x; e < nk32 * 256; e += NTHREADS)
-      *reinterpret_cast<uint4*>(sm + (size_t)e * 16) = __ldg(src + e);
+    if (geo.half) {
+      for (int e = threadIdx.x; e < nk32 * 128; e += NTHREADS)
+        *reinterpret_cast<uint4*>(sm + (size_t)e * 16) = __ldg(src + (e >> 7) * 256 + (e & 127));
+    } else {
+      for (int e = threadIdx.x; e < nk32 * 256; e += NTHREADS)
+        *reinterpret_cast<uint4*>(sm + (size_t)e * 16) = __ldg(src + e);
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -543,7 +563,7 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
           mbar_wait_backoff(&full_bar[s], sround & 1, 64);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           for (int k2 = 0; k2 < V2_KS && V2_KS * ch + k2 < nk32; k2++) {
-            const uint32_t aaddr = geo.wres ? sm_a + (uint32_t)(V2_KS * ch + k2) * 4096
+            const uint32_t aaddr = geo.wres ? sm_a + (uint32_t)(V2_KS * ch + k2) * (geo.half ? 2048u : 4096u)
                                             : sm_a + geo.off_a + (uint32_t)s * V2_STAGE_A + (uint32_t)k2 * 4096;
             const uint64_t da = umma_desc_kmajor(aaddr);
             const uint64_t db = umma_desc_kmajor(sm_a + geo.off_b + (uint32_t)s * V2_STAGE_B + (uint32_t)k2 * 8192);

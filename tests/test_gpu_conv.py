@@ -141,6 +141,21 @@ def test_conv_partial_units(hy):
         assert np.array_equal(got[i], ref[i])
 
 
+@pytest.mark.parametrize("batches", ["1", "2", "64"])
+def test_host_path_batches(hy, monkeypatch, batches):
+    """hy_conv_eval_host pipelined over several batches of units (HY_HOST_BATCHES forces the batch
+    count; the default policy keeps >= 32 MiB per batch, i.e. one batch at test sizes) returns the
+    device path's bytes; run_gpu compares host and device outputs."""
+    monkeypatch.setenv("HY_HOST_BATCHES", batches)
+    c = dict(CASES["cn1_blocks_tail"])
+    N, bits, L = c.pop("N"), c.pop("bits"), c.pop("L")
+    lay = make_layer(N, ntt_primes(N, bits, L), seed=551, **c)
+    got, _, Lay = run_gpu(hy, lay, shape_of(lay))
+    assert Lay.U >= 2
+    ref = conv.he_conv(lay.P, lay.ls, lay.W, lay.ct_in, lay.keys, out_cts=[0, Lay.Jout - 1])
+    assert np.array_equal(got[0], ref[0]) and np.array_equal(got[Lay.Jout - 1], ref[Lay.Jout - 1])
+
+
 def test_c1_config_full(hy):
     """BASELINE configs[0] (C1) end to end: full ciphertext parity + decryption."""
     lay = layer_from_config(synth.configs()["C1"])

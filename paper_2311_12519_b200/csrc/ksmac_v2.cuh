@@ -57,6 +57,9 @@
 #ifndef V2_PAD   // extra shared memory requested (experiment: less L1)
 #define V2_PAD 0
 #endif
+#ifndef V2_SHFL  // warp index through __shfl_sync (provably warp-uniform role branches)
+#define V2_SHFL 1
+#endif
 #ifndef V2_HALF  // M <= 64: resident weights as 64-row half tiles (more L1 for the digit windows)
 #define V2_HALF 1
 #endif
@@ -214,7 +217,13 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
   const int nk32 = a.Kpad / 32;
   const int nchunks = (nk32 + V2_KS - 1) / V2_KS;
   const int S = geo.S;
+  // warp index through a shuffle: ptxas then treats the role branches as warp-uniform (without it
+  // every global load in the producers re-materialised its memory descriptor with two R2UR)
+#if V2_SHFL
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+#else
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#endif
 
   // ---- setup (independent of the predecessor kernel: overlaps it under PDL) ----
   if (threadIdx.x == 0) {

@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(V3Warps<EPI>::THREADS, 1)
   const int nk32 = a.Kpad / 32;
   const int nchunks = (nk32 + V3_KS - 1) / V3_KS;
   const int S = geo.S;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;  // warp-uniform for ptxas (ksmac_v2.cuh)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; s++) {

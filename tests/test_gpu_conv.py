@@ -147,11 +147,11 @@ def test_host_path_batches(hy, monkeypatch, batches):
     count; the default policy keeps >= 32 MiB per batch, i.e. one batch at test sizes) returns the
     device path's bytes; run_gpu compares host and device outputs."""
     monkeypatch.setenv("HY_HOST_BATCHES", batches)
-    c = dict(CASES["cn1_blocks_tail"])
+    c = dict(CASES["cn1_blocks_tail"], batch=50)   # 4 units: batches of 4 / 2 / 1 units
     N, bits, L = c.pop("N"), c.pop("bits"), c.pop("L")
     lay = make_layer(N, ntt_primes(N, bits, L), seed=551, **c)
     got, _, Lay = run_gpu(hy, lay, shape_of(lay))
-    assert Lay.U >= 2
+    assert Lay.U == 4
     ref = conv.he_conv(lay.P, lay.ls, lay.W, lay.ct_in, lay.keys, out_cts=[0, Lay.Jout - 1])
     assert np.array_equal(got[0], ref[0]) and np.array_equal(got[Lay.Jout - 1], ref[Lay.Jout - 1])
 

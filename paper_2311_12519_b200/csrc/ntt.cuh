@@ -344,6 +344,9 @@ inline size_t ntt_smem_bytes() {
 #ifndef NTT2_Q1
 #define NTT2_Q1 0
 #endif
+#ifndef NTT2_LAZY  // forward transform: conditional subtraction on every other stage only (needs NTT2_PTX, not NTT2_APX); bit-exact, measured no faster (C4 S1 4.39 vs 4.37 ms): off
+#define NTT2_LAZY 0
+#endif
 #ifndef NTT2_EXP  // timing experiments only (wrong results), bit mask: 1 = no butterfly arithmetic, 2 = no global loads / stores, 4 = no twiddle loads
 #define NTT2_EXP 0
 #endif
@@ -416,6 +419,38 @@ __device__ __forceinline__ void ntt2_ct_ptx(u64& x, u64& y, u64 w, u64 ws, u64 n
       "mov.b64 %0, {x0, x1};\n\tmov.b64 %1, {y0, y1};\n\t}"
       : "+l"(x), "+l"(y)
       : "l"(w), "l"(ws), "l"(nq), "l"(q2));
+}
+
+// Forward butterfly with the conditional subtraction on every other stage only (NTT2_LAZY): a Shoup
+// product takes any 64-bit y, so the values may grow by 2q per stage: [0, 4q) in, no correction in
+// stages 0, 1 and every odd stage (values < 8q < 2^63), x mod' 4q in the even stages >= 2 (values
+// back below 6q); the output is normalised from [0, 8q).  cs is a compile-time constant after unrolling.
+__device__ __forceinline__ void ntt2_ct_lazy(u64& x, u64& y, u64 w, u64 ws, u64 nq, u64 q2, u64 q4, bool cs) {
+  if (cs) {
+    asm("{\n\t.reg .u32 x0, x1, y0, y1, w0, w1, s0, s1, n0, n1, t0, t1, f0, f1, a0, a1, a2, h0, h1, T0, T1, d0, d1, m;\n\t"
+        "mov.b64 {x0, x1}, %0;\n\tmov.b64 {y0, y1}, %1;\n\tmov.b64 {w0, w1}, %2;\n\tmov.b64 {s0, s1}, %3;\n\t"
+        "mov.b64 {n0, n1}, %4;\n\tmov.b64 {t0, t1}, %5;\n\tmov.b64 {f0, f1}, %6;\n\t"
+        NTT2_SHOUP_T("y0", "y1")
+        "sub.cc.u32 d0, x0, f0;\n\tsubc.cc.u32 d1, x1, f1;\n\tsubc.u32 m, 0, 0;\n\t"
+        "lop3.b32 x0, m, x0, d0, 0xCA;\n\tlop3.b32 x1, m, x1, d1, 0xCA;\n\t"
+        "add.cc.u32 d0, x0, t0;\n\taddc.u32 d1, x1, t1;\n\t"
+        "sub.cc.u32 y0, d0, T0;\n\tsubc.u32 y1, d1, T1;\n\t"
+        "add.cc.u32 x0, x0, T0;\n\taddc.u32 x1, x1, T1;\n\t"
+        "mov.b64 %0, {x0, x1};\n\tmov.b64 %1, {y0, y1};\n\t}"
+        : "+l"(x), "+l"(y)
+        : "l"(w), "l"(ws), "l"(nq), "l"(q2), "l"(q4));
+  } else {
+    asm("{\n\t.reg .u32 x0, x1, y0, y1, w0, w1, s0, s1, n0, n1, t0, t1, a0, a1, a2, h0, h1, T0, T1, d0, d1;\n\t"
+        "mov.b64 {x0, x1}, %0;\n\tmov.b64 {y0, y1}, %1;\n\tmov.b64 {w0, w1}, %2;\n\tmov.b64 {s0, s1}, %3;\n\t"
+        "mov.b64 {n0, n1}, %4;\n\tmov.b64 {t0, t1}, %5;\n\t"
+        NTT2_SHOUP_T("y0", "y1")
+        "add.cc.u32 d0, x0, t0;\n\taddc.u32 d1, x1, t1;\n\t"
+        "sub.cc.u32 y0, d0, T0;\n\tsubc.u32 y1, d1, T1;\n\t"
+        "add.cc.u32 x0, x0, T0;\n\taddc.u32 x1, x1, T1;\n\t"
+        "mov.b64 %0, {x0, x1};\n\tmov.b64 %1, {y0, y1};\n\t}"
+        : "+l"(x), "+l"(y)
+        : "l"(w), "l"(ws), "l"(nq), "l"(q2));
+  }
 }
 
 __device__ __forceinline__ void ntt2_gs_ptx(u64& x, u64& y, u64 w, u64 ws, u64 nq, u64 q2) {
@@ -503,21 +538,26 @@ __global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
 #pragma unroll
   for (int r = 0; r < V; r++) v[r] = (NTT2_EXP & 2) ? (u64)(tid + T * r) * q : jb.load(tid + T * r);
 #if NTT2_EXP & 1
-  auto bfly = [&](u64& x, u64& y, const ulonglong2 w) { x ^= y + w.x; y ^= w.y; };
+  auto bfly = [&](u64& x, u64& y, const ulonglong2 w, int) { x ^= y + w.x; y ^= w.y; };
+#elif NTT2_PTX && NTT2_LAZY && !NTT2_APX
+  const u64 nq = ntt2_nq(q), q4 = 4 * q;
+  auto bfly = [&](u64& x, u64& y, const ulonglong2 w, int st) {
+    ntt2_ct_lazy(x, y, w.x, w.y, nq, q2, q4, st >= 2 && (st & 1) == 0);
+  };
 #elif NTT2_PTX
   const u64 nq = ntt2_nq(q), qb = (NTT2_APX ? 5 : 2) * q;  // values in [0, 2 qb)
-  auto bfly = [&](u64& x, u64& y, const ulonglong2 w) { ntt2_ct_ptx(x, y, w.x, w.y, nq, qb); };
+  auto bfly = [&](u64& x, u64& y, const ulonglong2 w, int) { ntt2_ct_ptx(x, y, w.x, w.y, nq, qb); };
 #elif NTT2_APX
   // approximate Shoup quotient (umulhi_apx: Tt in [0, 5q)): values stay in [0, 10q) < 2^64 (q < 2^60)
   const u64 qb = 5 * q;
-  auto bfly = [&](u64& x, u64& y, const ulonglong2 w) {  // CT: [0, 10q) -> [0, 10q)
+  auto bfly = [&](u64& x, u64& y, const ulonglong2 w, int) {  // CT: [0, 10q) -> [0, 10q)
     const u64 X = csub2(x, qb);
     const u64 Tt = y * w.x - umulhi_apx(y, w.y) * q;
     x = X + Tt;
     y = X - Tt + qb;
   };
 #else
-  auto bfly = [&](u64& x, u64& y, const ulonglong2 w) {  // Harvey CT: [0, 4q) -> [0, 4q)
+  auto bfly = [&](u64& x, u64& y, const ulonglong2 w, int) {  // Harvey CT: [0, 4q) -> [0, 4q)
     const u64 X = csub2(x, q2);
     const u64 Tt = shoup_mul(y, w.x, w.y, q);
     x = X + Tt;
@@ -530,7 +570,7 @@ __global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
     const int h = 16 >> s;
 #pragma unroll
     for (int r = 0; r < V; r++)
-      if ((r & h) == 0) bfly(v[r], v[r + h], NTT2_TW(W + (1 << s) + (r >> (5 - s))));
+      if ((r & h) == 0) bfly(v[r], v[r + h], NTT2_TW(W + (1 << s) + (r >> (5 - s))), s);
   }
 #pragma unroll
   for (int r = 0; r < V; r++) sm[ntt2_sw<LOGN>(tid + T * r)] = v[r];
@@ -546,7 +586,7 @@ __global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
     const int sh = LOGN - s;  // log2 of the block size of stage s
 #pragma unroll
     for (int r = 0; r < V; r++)
-      if ((r & h) == 0) bfly(v[r], v[r + h], NTT2_TW(W + (1 << s) + (blk << (s - 5)) + ((D * r) >> sh)));
+      if ((r & h) == 0) bfly(v[r], v[r + h], NTT2_TW(W + (1 << s) + (blk << (s - 5)) + ((D * r) >> sh)), s);
   }
   // (every thread rewrites exactly the positions it read: no barrier before the write-back)
 #pragma unroll
@@ -567,7 +607,7 @@ __global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
       for (int rr = 0; rr < D; rr++)
         if ((rr & h) == 0)
           bfly(v[qq * D + rr], v[qq * D + rr + h],
-               NTT2_TW(W + (1 << s) + ((tid + T * qq) << (s - 10)) + (rr >> (LOGN - s))));
+               NTT2_TW(W + (1 << s) + ((tid + T * qq) << (s - 10)) + (rr >> (LOGN - s))), s);
   }
 #pragma unroll
   for (int qq = 0; qq < C::QN; qq++)
@@ -575,6 +615,8 @@ __global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
     for (int rr = 0; rr < D; rr++) {
 #if NTT2_APX
       const u64 x = csub2(csub2(csub2(csub2(v[qq * D + rr], 8 * q), 4 * q), q2), q);
+#elif NTT2_PTX && NTT2_LAZY
+      const u64 x = csub2(csub2(csub2(v[qq * D + rr], 4 * q), q2), q);
 #else
       const u64 x = csub2(csub2(v[qq * D + rr], q2), q);
 #endif

@@ -49,6 +49,35 @@ def test_poly_mul_matches_schoolbook(hy, N, bits, L):
         hy.hy_params_destroy(p)
 
 
+@pytest.mark.parametrize("N,bits,L", [(4096, 50, 2), (8192, 60, 3), (8192, 59, 2)])
+def test_throughput_ntt_kernels(hy, N, bits, L):
+    """Launches of >= 592 transforms take the one-CTA-per-transform kernels (ntt2_*: inline-PTX
+    butterflies, conditional subtraction on every other forward stage): products of edge-valued and
+    random polynomials against the schoolbook oracle, and NTT -> INTT = identity on all of them."""
+    primes = ntt_primes(N, bits, L)
+    p = hy.hy_params_create(N, primes, 65537)
+    try:
+        g = synth.rng(210 + L, "misc")
+        n = 600 // L + 8
+        a = synth.uniform_residues(g, primes, (n, N))
+        b = synth.uniform_residues(g, primes, (n, N))
+        for l, q in enumerate(primes):
+            a[0, l, :], b[0, l, :] = q - 1, q - 1          # largest residues everywhere
+            a[1, l, :], b[1, l, : N // 2] = q - 1, 0
+            a[2, l, :] = 0
+        da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+        dc = torch.empty_like(da)
+        hy.hy_poly_mul(p, da, db, dc)
+        c = dc.cpu().numpy()
+        for i in (0, 1, 2, 3, n - 1):
+            for l, q in enumerate(primes):
+                assert np.array_equal(c[i, l], ring.nc_mul(a[i, l], b[i, l], q)), (i, l)
+        hy.hy_ntt_roundtrip(p, da)
+        assert np.array_equal(da.cpu().numpy(), a)
+    finally:
+        hy.hy_params_destroy(p)
+
+
 @pytest.mark.parametrize("N,bits,L", PARAMS)
 def test_ntt_roundtrip(hy, N, bits, L):
     primes = ntt_primes(N, bits, L)

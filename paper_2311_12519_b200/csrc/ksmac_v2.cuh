@@ -57,6 +57,9 @@
 #ifndef V2_PAD   // extra shared memory requested (experiment: less L1)
 #define V2_PAD 0
 #endif
+#ifndef V2_KBCONST
+#define V2_KBCONST 1
+#endif
 #ifndef V2_SHFL  // warp index through __shfl_sync (provably warp-uniform role branches)
 #define V2_SHFL 1
 #endif
@@ -102,7 +105,7 @@ inline V2Geom v2_geom(int T, int L, int Kpad, size_t smem_max, int M = 128) {
   const uint32_t bar = 256;
   for (int wres = V2_WRES; wres >= 0; wres--) {
     for (int S = V2_SMAX; S >= 2; S--) {
-      for (int kb = V2_KBMAX; kb >= 3; kb--) {
+      for (int kb = V2_KBMAX; kb >= V2_KBMAX; kb--) {  // exactly V2_KBMAX buffers (compile-time count in the kernel)
         const uint32_t w = wres ? wbytes : 0;
         const uint32_t per = V2_STAGE_B + (wres ? 0 : V2_STAGE_A);
         const size_t tot = 1024 + (size_t)w + (size_t)S * per + (size_t)kb * g.key_bytes + bar + V2_PAD;
@@ -205,7 +208,13 @@ __global__ void __launch_bounds__(V2Warps<EPI>::THREADS, 1)
   uint64_t* const kfull = bars + 12;          // [kb] key buffer landed (cp.async arrivals)
   uint64_t* const kempty = bars + 16;         // [kb] key buffer no longer read
   uint32_t* const s_tmem = reinterpret_cast<uint32_t*>(bars + 20);
+#if V2_KBCONST  // v2_geom only ever returns V2_KBMAX key buffers: a compile-time count turns the per-tile
+  // `% KB`, `/ KB` (runtime integer divisions: ~150 SASS per tile and thread, 5% of all executed
+  // instructions in the ncu SASS view) into multiply-shift pairs
+  constexpr int KB = V2_KBMAX;
+#else
   const int KB = geo.kb;
+#endif
 
   constexpr bool CN = LOGN > 0;
   const int N = CN ? (1 << LOGN) : (1 << a.logN);

@@ -347,6 +347,9 @@ inline size_t ntt_smem_bytes() {
 #ifndef NTT2_LAZY  // forward transform: conditional subtraction on every other stage only (needs NTT2_PTX, not NTT2_APX); bit-exact, measured no faster (C4 S1 4.39 vs 4.37 ms): off
 #define NTT2_LAZY 0
 #endif
+#ifndef NTT2_MINB  // resident CTAs per SM asked of ptxas at N = 8192 (2: 128 registers; 3: 80 registers, spills)
+#define NTT2_MINB 2
+#endif
 #ifndef NTT2_EXP  // timing experiments only (wrong results), bit mask: 1 = no butterfly arithmetic, 2 = no global loads / stores, 4 = no twiddle loads
 #define NTT2_EXP 0
 #endif
@@ -522,7 +525,7 @@ struct Ntt2Tables {
 __device__ __forceinline__ u64 csub2(u64 x, u64 m) { return x >= m ? x - m : x; }
 
 template <int LOGN, class Job>
-__global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
+__global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? NTT2_MINB : 2 * NTT2_MINB))
     ntt2_fwd_kernel(Job job, Ntt2Tables tb, LimbConsts L) {
   pdl_begin();
   using C = Ntt2Cfg<LOGN>;
@@ -633,7 +636,7 @@ __global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
 }
 
 template <int LOGN, class Job>
-__global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? 2 : 4))
+__global__ void __launch_bounds__(Ntt2Cfg<LOGN>::T, (LOGN == 13 ? NTT2_MINB : 2 * NTT2_MINB))
     ntt2_inv_kernel(Job job, Ntt2Tables tb, LimbConsts L) {
   pdl_begin();
   using C = Ntt2Cfg<LOGN>;

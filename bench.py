@@ -448,7 +448,8 @@ def workload_name(cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 50; 10 for --impl reference, whose steps take seconds)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="hyena", choices=["hyena", "reference"])
@@ -456,6 +457,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--mac-path", default=None, help="A/B: force an S2+S3 kernel path (hyena.MAC_PATHS)")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 10 if getattr(args, "impl", None) == "reference" else 50
     assert args.warmup >= 3, "W >= 3 warm-up steps"
     cfg = synth.configs()[args.config]
     if args.impl == "reference":
